@@ -1,0 +1,346 @@
+"""Oracle pins, part 2: the whole estimator against closed forms, brute force
+and invariants — SURVEY.md §8(c) pins P1-P6 plus the edge cases of readings
+Q3-Q9.  Nothing here compares the oracle with itself through a retyped formula:
+expected values come from the analytic scene (plane normal, sphere normal),
+numpy's SVD (PlaneSVD, Eq. 2), exact symmetries, or SPEC's printed fixture."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import tfn_scenes as ts
+from oracle.metrics import angular_error_deg
+
+FILTERS = ("fd", "sobel", "scharr", "prewitt")
+MODES = ("mean", "median")
+
+
+def _ang(a, b):
+    """per-pixel angle (deg) between [3,H,W] maps."""
+    return angular_error_deg(np.moveaxis(a, 0, -1), np.moveaxis(b, 0, -1))
+
+
+def _valid(n):
+    return np.all(np.isfinite(n), axis=0)
+
+
+# ------------------------------------------------------------------ P1 closed form
+def test_p1_spec_slanted_plane(golden):
+    """plane x + z = 2, K=(1,1,0,0) -> [-0.7071,0,-0.7071] everywhere interior."""
+    fx = golden["slanted_plane"]
+    H, W = 6, 8
+    u = np.arange(W, dtype=float)[None, :].repeat(H, 0)
+    z = 2.0 / (1.0 + u)                      # x = u z (K=(1,1,0,0)) and x + z = 2
+    for f in FILTERS:
+        # the candidate value itself: inverse depth (u+1)/2 -> n_x = s/2 per kernel
+        x = 1.0 / z
+        gu, gv = oracle.gradient_at(x, 2, 3, f)
+        p = oracle.backproject(fx["K"], 3, 2, z[2, 3])
+        q = oracle.backproject(fx["K"], 4, 2, z[2, 4])
+        c = oracle.nz_candidate(p, q, fx["K"][0] * gu, fx["K"][1] * gv)
+        assert abs(c - fx["candidate_per_filter"][f]) < 1e-12, f
+        for m in MODES:
+            n = oracle.estimate(z, fx["K"], f, m)
+            inner = n[:, 1:-1, 1:-1].reshape(3, -1).T
+            np.testing.assert_allclose(inner, np.tile(fx["normal"], (inner.shape[0], 1)), atol=1e-12)
+
+
+@pytest.mark.parametrize("f", FILTERS)
+def test_p1_tilted_plane_analytic(f):
+    """Eq. 14: on a plane 1/z is affine in (u,v), so every kernel and
+    both Phi recover the exact camera-facing normal (fp64 analytic input)."""
+    K = ts.Intrinsics(60.0, 55.0, 31.5, 23.25)          # non-integer principal point
+    rng = np.random.default_rng(7)
+    for trial in range(3):
+        t = rng.uniform(0.1, 1.0)
+        a = rng.uniform(0, 2 * math.pi)
+        n_true = np.array([math.sin(t) * math.cos(a), math.sin(t) * math.sin(a), -math.cos(t)])
+        sc = ts.plane_scene(n_true, (0, 0, rng.uniform(2, 5)))
+        r = ts.render(sc, K, 48, 64, keep_depth64=True)
+        d64 = r.depth64[0].numpy()
+        for m in MODES:
+            n = oracle.estimate(d64, K, f, m)
+            ok = _valid(n)
+            assert ok[1:-1, 1:-1].all()
+            err = _ang(n, np.broadcast_to(n_true[:, None, None], n.shape))[ok]
+            assert err.max() < 1e-9, (f, m, err.max())
+
+
+def test_p1_plane_fp32_input_bound():
+    """fp32-quantised plane (480x640): error vs analytic is input quantisation only,
+    bounded by 1e-2 deg (SURVEY P1 measured 2-8e-3 deg)."""
+    n_true = np.array([0.3, -0.2, -1.0]); n_true /= np.linalg.norm(n_true)
+    sc = ts.plane_scene(n_true, (0, 0, 3))
+    r = ts.render(sc, ts.K_VGA, 480, 640)
+    for f in ("fd", "sobel"):
+        n = oracle.estimate(r.depth[0].numpy(), ts.K_VGA, f, "median")
+        ok = _valid(n)
+        err = _ang(n, np.broadcast_to(n_true[:, None, None], n.shape))[ok]
+        assert err.max() < 1e-2, err.max()
+
+
+def test_q6_axis_aligned_plane_skips_equal_neighbours():
+    """A plane with n_x = 0 has exactly equal depths along each row (dz = 0): those
+    candidates must be skipped (Q6) and the result is still the exact normal."""
+    n_true = np.array([0.0, -0.4, -1.0]); n_true /= np.linalg.norm(n_true)
+    K = ts.Intrinsics(100.0, 100.0, 32.0, 24.0)
+    r = ts.render(ts.plane_scene(n_true, (0, 0, 3)), K, 48, 64, keep_depth64=True)
+    d = r.depth64[0].numpy()
+    assert np.all(d[:, 1:] == d[:, :-1])                 # rows constant -> E/W dz == 0
+    for f in FILTERS:
+        for m in MODES:
+            n = oracle.estimate(d, K, f, m)
+            err = _ang(n, np.broadcast_to(n_true[:, None, None], n.shape))[_valid(n)]
+            assert err.max() < 1e-9
+
+
+# ------------------------------------------------------------------ P2 / P3 flat rule
+@pytest.mark.parametrize("f", FILTERS)
+@pytest.mark.parametrize("m", MODES)
+def test_p2_fronto_parallel_flat_rule(f, m):
+    z = np.full((9, 11), 2.5, dtype=np.float32)
+    n = oracle.estimate(z, ts.K_VGA, f, m)
+    assert np.isnan(n[:, 0, :]).all() and np.isnan(n[:, :, -1]).all()     # Q3 border
+    inner = n[:, 1:-1, 1:-1]
+    assert (inner[0] == 0).all() and (inner[1] == 0).all() and (inner[2] == -1).all()
+
+
+@pytest.mark.parametrize("m", MODES)
+def test_p3_on_axis_sphere_apex(m):
+    """a sphere centred on the optical axis -> exactly [0,0,-1] at the
+    principal point (symmetric render; Q9 + Q10 make the zero gradient exact)."""
+    K = ts.Intrinsics(500.0, 500.0, 320.0, 240.0)
+    r = ts.render(ts.sphere_scene((0, 0, 3), 1.0), K, 480, 641)
+    z = r.depth[0].numpy()
+    assert np.array_equal(z[:, 320 - 5:320], z[:, 321:326][:, ::-1])   # mirror-symmetric input
+    for f in FILTERS:
+        n = oracle.estimate(z[235:246, 315:326], ts.Intrinsics(500, 500, 5, 5), f, m)
+        assert tuple(n[:, 5, 5]) == (0.0, 0.0, -1.0), (f, m, n[:, 5, 5])
+
+
+# ------------------------------------------------------------------ P4 sphere vs GT
+def _sphere_errors(scale: int, mode: str, f: str):
+    K = ts.Intrinsics(500.0 * scale, 500.0 * scale, 320.0 * scale, 240.0 * scale)
+    H, W = 480 * scale, 640 * scale
+    r = ts.render(ts.config1_scene(), K, H, W)
+    n = oracle.estimate(r.depth[0].numpy(), K, f, mode)
+    sph = (r.obj[0].numpy() == 2)
+    # sphere pixels >= 3*scale px from any discontinuity (7x7 window all sphere)
+    k = 3 * scale
+    core = np.ones_like(sph)
+    for dv in range(-k, k + 1):
+        for du in range(-k, k + 1):
+            core &= np.roll(np.roll(sph, dv, 0), du, 1)
+    core[:k] = core[-k:] = False
+    core[:, :k] = core[:, -k:] = False
+    gt = r.gt[0].numpy().astype(np.float64)
+    return _ang(n, gt)[core & _valid(n)]
+
+
+def test_p4_sphere_accuracy_bounds_and_convergence():
+    """Method behaviour on curvature: stated bounds
+    at 480x640 and the error shrinking when the resolution doubles (same FOV)."""
+    e1 = _sphere_errors(1, "median", "fd")
+    assert e1.mean() <= 0.02 and np.percentile(e1, 99) <= 0.3, (e1.mean(), np.percentile(e1, 99))
+    m1 = _sphere_errors(1, "mean", "fd")
+    assert m1.mean() <= 0.6, m1.mean()
+    e2 = _sphere_errors(2, "median", "fd")
+    m2 = _sphere_errors(2, "mean", "fd")
+    assert e2.mean() <= 0.6 * e1.mean(), (e1.mean(), e2.mean())
+    assert m2.mean() <= 0.6 * m1.mean(), (m1.mean(), m2.mean())
+    assert np.percentile(m2, 99) <= 0.6 * np.percentile(m1, 99)
+
+
+def test_p4_median_beats_mean_on_clean_sphere():
+    """P:795 / S:609: the median is more accurate than the mean on clean data."""
+    for f in FILTERS:
+        assert _sphere_errors(1, "median", f).mean() <= _sphere_errors(1, "mean", f).mean() + 0.1
+
+
+# ------------------------------------------------------------------ P5 invariants
+@pytest.fixture(scope="module")
+def scene1():
+    return ts.render(ts.config1_scene(), ts.K_VGA, 120, 160, keep_depth64=True)
+
+
+def test_p5_unit_norm_and_camera_facing(scene1):
+    z = scene1.depth[0].numpy()
+    for f in FILTERS:
+        for m in MODES:
+            n = oracle.estimate(z, ts.K_VGA, f, m)
+            ok = _valid(n)
+            assert np.abs(np.sqrt((n[:, ok] ** 2).sum(0)) - 1).max() < 1e-12
+            v, u = np.nonzero(ok)
+            zz = z[ok].astype(np.float64)
+            p = np.stack([(u - ts.K_VGA.u0) * zz / ts.K_VGA.fx, (v - ts.K_VGA.v0) * zz / ts.K_VGA.fy, zz])
+            assert ((n[:, ok] * p).sum(0) <= 0).all()
+
+
+def test_p5_kernel_scale_and_negation(scene1):
+    z = scene1.depth[0].numpy()
+    for m in MODES:
+        base = oracle.estimate(z, ts.K_VGA, (1.0, 2.0), m)
+        scaled = oracle.estimate(z, ts.K_VGA, (1.0 * 0.37, 2.0 * 0.37), m)
+        neg = oracle.estimate(z, ts.K_VGA, (-1.0, -2.0), m)
+        ok = _valid(base)
+        assert np.array_equal(ok, _valid(scaled)) and np.array_equal(ok, _valid(neg))
+        assert _ang(base, scaled)[ok].max() < 1e-9
+        assert np.array_equal(base[:, ok], neg[:, ok])        # negation is exact
+
+
+def test_p5_transpose_symmetry(scene1):
+    z = scene1.depth[0].numpy()
+    K = ts.K_VGA
+    Kt = ts.Intrinsics(K.fy, K.fx, K.v0, K.u0)
+    for f in FILTERS:
+        for m in MODES:
+            n = oracle.estimate(z, K, f, m)
+            nt = oracle.estimate(np.ascontiguousarray(z.T), Kt, f, m)
+            back = np.stack([nt[1].T, nt[0].T, nt[2].T])
+            ok = _valid(n)
+            assert np.array_equal(ok, _valid(back))
+            if m == "median":
+                assert np.array_equal(n[:, ok], back[:, ok])
+            else:
+                assert _ang(n, back)[ok].max() < 1e-9
+
+
+def test_p5_mean_equals_median_on_planes():
+    n_true = np.array([0.25, 0.4, -1.0]); n_true /= np.linalg.norm(n_true)
+    r = ts.render(ts.plane_scene(n_true, (0, 0, 4)), ts.K_VGA, 60, 80, keep_depth64=True)
+    for f in FILTERS:
+        a = oracle.estimate(r.depth64[0].numpy(), ts.K_VGA, f, "mean")
+        b = oracle.estimate(r.depth64[0].numpy(), ts.K_VGA, f, "median")
+        assert _ang(a, b)[_valid(a)].max() < 1e-9
+
+
+def test_p5_depth_equals_disparity_and_bf_cancels(scene1):
+    """Eq. 19-21: the disparity path is the depth path up to a positive factor
+    (<= 1e-4 deg); f*t_c only enters through z = f t_c / d."""
+    K = ts.K_VGA
+    d64 = scene1.depth64[0].numpy()
+    disp = np.where(d64 > 0, 500.0 * 0.12 / np.where(d64 > 0, d64, 1.0), 0.0)
+    z = np.where(disp > 0, 500.0 * 0.12 / np.where(disp > 0, disp, 1.0), 0.0)
+    for f in ("fd", "scharr"):
+        for m in MODES:
+            nd = oracle.estimate(z, K, f, m)
+            nq = oracle.estimate(disp, K, f, m, disparity=True, f_tc=500.0 * 0.12)
+            nb = oracle.estimate(disp, K, f, m, disparity=True, f_tc=500.0 * 0.12 * 73.0)
+            ok = _valid(nd)
+            assert np.array_equal(ok, _valid(nq))
+            assert _ang(nd, nq)[ok].max() < 1e-4
+            assert _ang(nq, nb)[ok].max() < 1e-6
+
+
+def test_p5_depth_scale_invariance(scene1):
+    z32 = scene1.depth[0].numpy()
+    d64 = scene1.depth64[0].numpy()
+    for m in MODES:
+        a = oracle.estimate(z32, ts.K_VGA, "sobel", m)
+        b = oracle.estimate(z32 * np.float32(4.0), ts.K_VGA, "sobel", m)      # power of two: exact
+        ok = _valid(a)
+        assert np.array_equal(a[:, ok], b[:, ok])
+        c = oracle.estimate(d64, ts.K_VGA, "sobel", m)
+        e = oracle.estimate(d64 * 3.0, ts.K_VGA, "sobel", m)                  # fp64 input, any s
+        ok = _valid(c)
+        assert _ang(c, e)[ok].max() < 1e-6
+
+
+# ------------------------------------------------------------------ P6 brute-force LSQ
+def test_p6_planesvd_brute_force():
+    """PlaneSVD (Eq. 1-2) on tiny planar images: the smallest
+    right singular vector of [Q+ 1] is the exact plane, and the oracle must agree."""
+    rng = np.random.default_rng(11)
+    worst = 0.0
+    for trial in range(120):
+        H, W = int(rng.integers(3, 7)), int(rng.integers(3, 7))
+        K = ts.Intrinsics(rng.uniform(50, 500), rng.uniform(50, 500), rng.uniform(0, W), rng.uniform(0, H))
+        t = rng.uniform(0, 1.0)
+        a = rng.uniform(0, 2 * math.pi)
+        n_true = np.array([math.sin(t) * math.cos(a), math.sin(t) * math.sin(a), -math.cos(t)])
+        r = ts.render(ts.plane_scene(n_true, (0, 0, rng.uniform(1, 6))), K, H, W, keep_depth64=True)
+        z = r.depth64[0].numpy()
+        f = FILTERS[trial % 4]
+        m = MODES[(trial // 4) % 2]
+        n = oracle.estimate(z, K, f, m)
+        for v in range(1, H - 1):
+            for u in range(1, W - 1):
+                pts = []
+                for dv in (-1, 0, 1):
+                    for du in (-1, 0, 1):
+                        zz = z[v + dv, u + du]
+                        pts.append([(u + du - K.u0) * zz / K.fx, (v + dv - K.v0) * zz / K.fy, zz, 1.0])
+                _, _, Vt = np.linalg.svd(np.array(pts))
+                b = Vt[-1]
+                nn = b[:3] / np.linalg.norm(b[:3])
+                pc = np.array(pts[4][:3])
+                if nn @ pc > 0:
+                    nn = -nn
+                e = angular_error_deg(n[:, v, u], nn)
+                worst = max(worst, float(e))
+    assert worst < 1e-8, worst
+
+
+# ------------------------------------------------------------------ edge cases Q3-Q9
+def test_q4_hole_neighbourhoods():
+    """Z=0 pixel: Sobel/Scharr/Prewitt invalidate its whole 3x3; FD only the plus
+    shape — its corner neighbours stay valid with that candidate skipped (Q4, Q6)."""
+    n_true = np.array([0.2, 0.1, -1.0]); n_true /= np.linalg.norm(n_true)
+    r = ts.render(ts.plane_scene(n_true, (0, 0, 3)), ts.K_VGA, 12, 14, keep_depth64=True)
+    z = r.depth64[0].numpy().copy()
+    z[5, 6] = 0.0
+    for f in FILTERS:
+        for m in MODES:
+            n = oracle.estimate(z, ts.K_VGA, f, m)
+            ok = _valid(n)
+            assert not ok[5, 6]
+            nb = [(5 + dv, 6 + du) for dv in (-1, 0, 1) for du in (-1, 0, 1) if (dv, du) != (0, 0)]
+            for (vv, uu) in nb:
+                corner = (vv != 5 and uu != 6)
+                expect_valid = (f == "fd" and corner)
+                assert ok[vv, uu] == expect_valid, (f, vv, uu)
+            err = _ang(n, np.broadcast_to(n_true[:, None, None], n.shape))[ok]
+            assert err.max() < 1e-9                        # skipping keeps the plane exact
+
+
+@pytest.mark.parametrize("bad", [0.0, -2.0, float("nan"), float("inf"), -float("inf"), 1e-45])
+def test_q5_invalid_samples(bad):
+    z = np.full((7, 7), 2.0, dtype=np.float32)
+    z[3, 3] = np.float32(bad)
+    n = oracle.estimate(z, ts.K_VGA, "sobel", "median")
+    ok = _valid(n)
+    assert not ok[2:5, 2:5].any()
+    assert ok[1, 1] and ok[5, 5]
+
+
+def test_q9_k_zero_is_flat():
+    """FD: plus-neighbours equal to the centre, corners invalid -> no candidate
+    and g = 0 -> [0,0,-1]."""
+    z = np.zeros((3, 3)); z[1, :] = 2.0; z[:, 1] = 2.0
+    n = oracle.estimate(z, ts.K_VGA, "fd", "median")
+    assert tuple(n[:, 1, 1]) == (0.0, 0.0, -1.0)
+
+
+def test_tiny_images_all_invalid():
+    for H, W in ((1, 1), (2, 5), (5, 2)):
+        n = oracle.estimate(np.full((H, W), 2.0, np.float32), ts.K_VGA, "fd", "mean")
+        assert np.isnan(n).all()
+
+
+def test_disparity_requires_single_focal_length():
+    with pytest.raises(ValueError):
+        oracle.estimate(np.ones((4, 4), np.float32), ts.Intrinsics(500, 501, 2, 2), "fd", "mean",
+                        disparity=True, f_tc=1.0)
+
+
+def test_pixel_entry_matches_frame(scene1):
+    z = scene1.depth[0].numpy()
+    full = oracle.estimate(z, ts.K_VGA, "sobel", "median")
+    rng = np.random.default_rng(3)
+    pix = [(0, 5), (119, 3), (60, 0), (60, 159)] + [tuple(x) for x in rng.integers(0, (120, 160), (200, 2))]
+    one = oracle.estimate_pixels(z, ts.K_VGA, pix, "sobel", "median")
+    for (v, u), n in zip(pix, one):
+        a = full[:, v, u]
+        assert (np.isnan(a).all() and np.isnan(n).all()) or np.array_equal(a, n)
