@@ -1,0 +1,437 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the B200-native 3F2N hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl tfn|reference]
+
+A step is one pass of the whole hot path (one fused
+kernel launch) over one batch of synthetic frames resident in HBM.  Default
+workload = BASELINE.json configs[1]: 1024 x 480x640 depth frames, Sobel + median,
+planar fp32 normals, per GPU (weak scaling: each rank renders its own frames).
+Inputs (1.26 GB) exceed the 126 MB L2, so no flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the fp64 CPU oracle
+(oracle/, the only non-test code allowed to run it) on the same config/metric.
+Multi-GPU: torchrun; per-rank timing with CUDA events, max over ranks; NCCL only
+all-reduces the int64 angular-error statistics (off the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import tfn_scenes as ts  # noqa: E402
+
+METRIC = "Mpixel/s and 480×640 frames/s per B200 and at 2/4/8 GPUs; % HBM roofline"
+BYTES_PER_PX = 16  # 4 B fp32 sample read + 12 B fp32 normal written
+
+CONFIGS = {
+    # id: (frames per rank, H, W, K, filter, mode, input, holes/salt, description)
+    1: dict(frames=1, H=480, W=640, K=ts.K_VGA, filter="sobel", mode="mean", disp=False, holes=False,
+            desc="1 x 480x640 tilted plane + sphere, Sobel + mean (configs[0])", scene="config1"),
+    2: dict(frames=1024, H=480, W=640, K=ts.K_VGA, filter="sobel", mode="median", disp=False, holes=False,
+            desc="1024 x 480x640 random plane+sphere depth frames, Sobel + median (configs[1])", scene="random"),
+    3: dict(frames=1024, H=480, W=640, K=ts.K_VGA, filter="scharr", mode="median", disp=True, holes=False,
+            desc="1024 x 480x640 disparity (f=500, b=0.12), Scharr + median (configs[2])", scene="random"),
+    4: dict(frames=128, H=1080, W=1920, K=ts.K_1080, filter="prewitt", mode="median", disp=False, holes=True,
+            desc="128 x 1080x1920 depth with Z=0 holes, Prewitt + median (configs[3])", scene="random"),
+    5: dict(frames=65536, H=480, W=640, K=ts.K_VGA, filter="sobel", mode="median", disp=False, holes=False,
+            desc="65536 x 480x640 streamed in 1024-frame chunks, sharded over ranks (configs[4])",
+            scene="random", stream=True),
+}
+BASELINE_F = 500.0
+BASELINE_B = 0.12
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="tfn", choices=["tfn", "reference"])
+    ap.add_argument("--filter", default=None)
+    ap.add_argument("--mode", default=None)
+    ap.add_argument("--layout", default="planar", choices=["planar", "packed"])
+    ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel"])
+    ap.add_argument("--strip-h", type=int, default=0)
+    ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--no-streaming-stores", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/stats)")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(cfg_id, filt, mode, layout):
+    """dram bytes/launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(f"config{cfg_id}:{filt}:{mode}:{layout}")
+        return e
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.nv = None
+
+    _REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self._REASONS.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def make_frames(cfg, n, first, seed, device):
+    """Render n frames (global ids first..first+n-1) on `device`: (input f32, GT f32)."""
+    H, W, K = cfg["H"], cfg["W"], cfg["K"]
+    if cfg["scene"] == "config1":
+        sc = ts.config1_scene()
+        r = ts.render(sc, K, H, W, device=device, keep_depth64=cfg["disp"])
+        reps = n
+        depth = r.depth.expand(reps, H, W).contiguous()
+        gt = r.gt.expand(reps, 3, H, W).contiguous()
+        d64 = r.depth64
+    else:
+        sc = ts.random_scenes(n, K, H, W, seed=seed, first_frame=first, holes=cfg["holes"],
+                              salt=0.01 if cfg["holes"] else 0.0)
+        chunk = max(1, int(2.0e8 // (H * W * 8)))
+        ds, gs = [], []
+        for lo in range(0, n, chunk):
+            hi = min(n, lo + chunk)
+            r = ts.render(sc.subset(lo, hi), K, H, W, device=device, keep_depth64=cfg["disp"])
+            if cfg["disp"]:
+                ds.append(ts.depth_to_disparity(r.depth64, BASELINE_F, BASELINE_B))
+            else:
+                ds.append(r.depth)
+            gs.append(r.gt)
+            del r
+        depth = torch.cat(ds)
+        gt = torch.cat(gs)
+        return depth, gt
+    if cfg["disp"]:
+        depth = ts.depth_to_disparity(d64, BASELINE_F, BASELINE_B).expand(n, H, W).contiguous()
+    return depth, gt
+
+
+# ------------------------------------------------------------------ reference arm (oracle)
+def run_reference(args, cfg, ws, rank):
+    if rank != 0:
+        return 0
+    import oracle
+    filt = args.filter or cfg["filter"]
+    mode = args.mode or cfg["mode"]
+    H, W = cfg["H"], cfg["W"]
+    cores = os.cpu_count() or 1
+    # a bounded sample of the workload per step: `cores` frames (one per thread)
+    n = cores
+    depth, _ = make_frames(cfg, n, 0, args.seed, "cpu")
+    x = depth.numpy()
+    kw = dict(disparity=cfg["disp"], f_tc=BASELINE_F * BASELINE_B)
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle.estimate(x, cfg["K"], filt, mode, threads=cores, **kw)
+    times = []
+    steps = max(1, min(args.steps, 5))
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.estimate(x, cfg["K"], filt, mode, threads=cores, **kw)
+        times.append(time.perf_counter() - t0)
+    t = float(np.sum(times))
+    px = n * H * W * steps
+    val = px / t / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "Mpixel/s", "n_gpus": ws,
+        "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * t / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded analytic ray-cast scenes)",
+        "config": {"workload": cfg["desc"], "filter": filt, "nz_mode": mode, "H": H, "W": W,
+                   "frames_per_step": n, "fps": val * 1e6 / (H * W)},
+        "cpu_baseline": {"value": val, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{n} frames/step ({H}x{W}), {steps} steps, fp64 C oracle, one frame per thread"},
+        "e2e": {"value": val, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(cfg, filt, mode, seconds, seed):
+    """The oracle as it stands on this host's cores, on a bounded sample of the workload."""
+    import oracle
+    H, W = cfg["H"], cfg["W"]
+    cores = os.cpu_count() or 1
+    d1, _ = make_frames(cfg, 1, 0, seed, "cpu")
+    kw = dict(disparity=cfg["disp"], f_tc=BASELINE_F * BASELINE_B)
+    t0 = time.perf_counter()
+    oracle.estimate(d1.numpy(), cfg["K"], filt, mode, **kw)
+    t1 = time.perf_counter() - t0
+    n = int(max(cores, min(cfg["frames"], round(seconds * cores / max(t1, 1e-3)))))
+    n = (n // cores) * cores or cores
+    depth, _ = make_frames(cfg, n, 0, seed, "cpu")
+    x = depth.numpy()
+    t0 = time.perf_counter()
+    oracle.estimate(x, cfg["K"], filt, mode, threads=cores, **kw)
+    t = time.perf_counter() - t0
+    val = n * H * W / t / 1e6
+    return {"value": val, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n} frames of the workload ({H}x{W}, {filt}+{mode}), fp64 C oracle, "
+                      f"frames split over {cores} threads, {t:.1f} s"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    cfg = dict(CONFIGS[args.config])
+    if args.frames:
+        cfg["frames"] = args.frames
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, cfg, ws, rank)
+
+    import paper_2005_08165_b200 as tfn
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    filt = args.filter or cfg["filter"]
+    mode = args.mode or cfg["mode"]
+    H, W, K = cfg["H"], cfg["W"], cfg["K"]
+    streaming_cfg = cfg.get("stream", False)
+    per_rank = cfg["frames"] // ws if streaming_cfg else cfg["frames"]
+    chunk = min(per_rank, 1024) if streaming_cfg else per_rank
+    first = rank * per_rank
+
+    est = tfn.Estimator(K, filter=filt, nz_mode=mode, layout=args.layout, kernel=args.kernel,
+                        strip_h=args.strip_h, grid=args.grid, streaming=not args.no_streaming_stores)
+    stream = torch.cuda.current_stream(dev)
+
+    def launch(x, out):
+        if cfg["disp"]:
+            est.estimate_disparity(x, BASELINE_F * BASELINE_B, out=out, stream=stream)
+        else:
+            est.estimate(x, out=out, stream=stream)
+
+    x, gt = make_frames(cfg, chunk, first, args.seed, dev)
+    out = torch.empty((chunk, 3, H, W) if args.layout == "planar" else (chunk, H, W, 3),
+                      dtype=torch.float32, device=dev)
+    torch.cuda.synchronize()
+    for _ in range(max(args.warmup, 3 if not args.profile else args.warmup)):
+        launch(x, out)
+    torch.cuda.synchronize()
+
+    steps = args.steps
+    n_chunks = (per_rank + chunk - 1) // chunk if streaming_cfg else 1
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    launches0 = tfn.tfn_kernel_launches()
+    acc = torch.zeros(8, dtype=torch.int64, device=dev)
+    clk = ClockSampler(local)
+    if streaming_cfg:
+        # config 5: per rank, chunks of 1024 frames: render (untimed) -> estimate (timed) -> stats
+        steps = n_chunks
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        kernel_ms = 0.0
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+        with clk:
+            for c in range(n_chunks):
+                lo = first + c * chunk
+                n = min(chunk, first + per_rank - lo)
+                if c > 0:
+                    x, gt = make_frames(cfg, n, lo, args.seed, dev)
+                    if out.shape[0] != n:
+                        out = out[:n]
+                torch.cuda.synchronize()
+                ev[c][0].record(stream)
+                launch(x, out)
+                ev[c][1].record(stream)
+                tfn.stats(out, gt, layout=args.layout, acc=acc, stream=stream)
+            torch.cuda.synchronize()
+        kernel_ms = sum(a.elapsed_time(b) for a, b in ev)
+        total_ms = kernel_ms
+        units = per_rank * H * W
+    else:
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+        t_all0 = torch.cuda.Event(enable_timing=True)
+        t_all1 = torch.cuda.Event(enable_timing=True)
+        with clk:
+            t_all0.record(stream)
+            for s in range(steps):
+                ev[s][0].record(stream)
+                launch(x, out)
+                ev[s][1].record(stream)
+            t_all1.record(stream)
+            torch.cuda.synchronize()
+        if pg:
+            pg.barrier()
+        total_ms = t_all0.elapsed_time(t_all1)
+        kernel_ms = sum(a.elapsed_time(b) for a, b in ev)
+        units = per_rank * H * W * steps
+    launches = tfn.tfn_kernel_launches() - launches0
+
+    t_max = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if pg:
+        pg.all_reduce(t_max, op=pg.ReduceOp.MAX)
+    total_ms_max = float(t_max.item())
+    all_units = units * ws
+    value = all_units / (total_ms_max / 1e3) / 1e6           # Mpixel/s whole job
+    per_launch_ms = kernel_ms / steps
+    px_per_launch = (chunk if not streaming_cfg else chunk) * H * W
+    achieved = BYTES_PER_PX * px_per_launch / (per_launch_ms / 1e3) / 1e9
+    peak, peak_kind = load_peaks()
+
+    # a8 accuracy statistics vs analytic GT (off the timed region), NCCL all-reduce of int64
+    if not streaming_cfg and not args.profile:
+        tfn.stats(out, gt, layout=args.layout, acc=acc, stream=stream)
+    if pg:
+        pg.all_reduce(acc)
+    st = acc.cpu().numpy().astype(np.int64)
+    m = int(st[1])
+    accuracy = None
+    if m > 0:
+        accuracy = {"aae_deg": st[0] / 1e6 / m, "pgp10": st[2] / m, "pgp20": st[3] / m, "pgp30": st[4] / m,
+                    "m": m, "stats_int64": [int(v) for v in st]}
+
+    # e2e through the public host-buffer API (pinned host in/out, H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e and not args.profile and not streaming_cfg:
+        hin = x.cpu().pin_memory()
+        hout = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
+        bf = BASELINE_F * BASELINE_B
+        est.estimate_host(hin, is_disparity=cfg["disp"], baseline_times_f=bf, out=hout)
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            est.estimate_host(hin, is_disparity=cfg["disp"], baseline_times_f=bf, out=hout)
+        dt = time.perf_counter() - t0
+        # wall clock of a blocking host->device->host call; max over ranks
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        if pg:
+            pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        dt = float(tt.item())
+        e2e = {"value": per_rank * H * W * args.e2e_steps * ws / dt / 1e6, "unit": "Mpixel/s",
+               "h2d_bytes_per_step": int(hin.numel() * 4), "d2h_bytes_per_step": int(hout.numel() * 4),
+               "api": "tfn_estimate_host (pinned host buffers, chunked H2D/kernel/D2H on 2 streams)"}
+        del hin, hout
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu and not args.profile:
+        cpu = cpu_baseline(cfg, filt, mode, args.cpu_seconds, args.seed)
+
+    if rank == 0:
+        traffic = load_traffic(args.config, filt, mode, args.layout)
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": ws, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": total_ms_max / steps, "higher_is_better": True,
+            "scaling": "weak" if not streaming_cfg else "strong", "vs_baseline": None,
+            "dtype": "f32 (fp64 gradient path)", "data": "synthetic (seeded analytic ray-cast scenes)",
+            "config": {"workload": cfg["desc"], "filter": filt, "nz_mode": mode, "layout": args.layout,
+                       "input": "disparity" if cfg["disp"] else "depth", "frames_per_gpu": per_rank,
+                       "H": H, "W": W, "fps": value * 1e6 / (H * W),
+                       "l2": "inputs (%.2f GB/GPU) larger than the 126 MB L2; no flush" % (chunk * H * W * 4 / 1e9),
+                       "parallelism": f"dp{ws} (frame batches sharded, no collective on the hot path)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                         "kernel": "tfn_strip_kernel", "bytes_per_px": BYTES_PER_PX,
+                         "px_per_launch": px_per_launch, "launch_ms": per_launch_ms},
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+            "cpu_baseline": cpu, "accuracy_vs_gt": accuracy,
+        }
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

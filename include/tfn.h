@@ -1,0 +1,137 @@
+/*
+ * tfn.h — C ABI of the B200-native 3F2N ("three-filters-to-normal") surface-normal
+ * estimator: libtfn.so (paper_2005_08165_b200/libtfn.so), sm_100a only.
+ *
+ * The operation (§III): for every
+ * pixel (u = column, v = row, 0-based) of a batch of depth images Z (or disparity
+ * images d), with pinhole intrinsics K = (fx, fy, u0, v0) (Eq. 13):
+ *   1. g_u, g_v = horizontal / vertical gradient filter (FD, Sobel, Scharr or
+ *      Prewitt) of the inverse depth 1/Z (disparity: of d, Eq. 21);
+ *   2. n_x = fx g_u, n_y = fy g_v  (Eq. 18; disparity Eq. 21: n_x = g_u, n_y = g_v);
+ *   3. n_z = -Phi_j{ (dX_j n_x + dY_j n_y) / dZ_j } over the 8-neighbourhood, the
+ *      neighbours back-projected with K (Eq. 13, 17, 18), Phi = mean or median
+ *      (P:218), skipping invalid neighbours and dZ_j == 0;
+ *   4. flat rule: g_u == g_v == 0 -> n = [0,0,-1];
+ *   5. n normalised and oriented toward the camera (<n, p> <= 0).
+ * The readings of everything the paper leaves open (validity, border, even-count
+ * median, orientation tie, ...) are DESIGN.md §3 (Q1-Q19); they are identical to
+ * the fp64 oracle's (oracle/tfn_oracle.c).
+ *
+ * Data layout.  Inputs are contiguous fp32 [batch, H, W] row-major.  A sample is
+ * VALID iff it is finite and >= FLT_MIN (zero, negative, NaN, Inf and fp32
+ * subnormals mean "no measurement").  Outputs are fp32 unit normals:
+ *   TFN_LAYOUT_PLANAR  [batch, 3, H, W]  (n_x plane, n_y plane, n_z plane)
+ *   TFN_LAYOUT_PACKED  [batch, H, W, 3]
+ * An output pixel is VALID iff it is not on the 1-pixel image border, its centre
+ * sample is valid and every tap with a nonzero weight in either gradient kernel is
+ * valid (FD: the 4 edge neighbours; Sobel/Scharr/Prewitt: all 8).  Invalid output
+ * pixels are written as (NaN, NaN, NaN) — invalid pixels are data, not errors.
+ *
+ * Ownership.  The caller owns every buffer.  Device pointers must be cudaMalloc'd
+ * (or torch) memory on the current device; inputs and outputs must not overlap.
+ * 16-byte-aligned buffers with W % 4 == 0 take the strip kernel (the fast path);
+ * anything else (>= 4-byte aligned) takes the per-pixel kernel, same results.
+ * A handle holds only its parameters (plus, for tfn_estimate_host, a lazily
+ * allocated device workspace guarded by a mutex); set options before the first
+ * estimate.  Device calls are asynchronous on `stream` (a cudaStream_t passed as
+ * void*; NULL = legacy default stream); kernel faults surface at the caller's
+ * next synchronisation.  batch == 0 is a no-op returning TFN_OK.  H or W < 3 is
+ * valid and yields an all-invalid (NaN) output.
+ *
+ * Errors: every entry point returns a tfn_status; nothing is thrown or printed.
+ */
+#ifndef TFN_H
+#define TFN_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TFN_OK = 0,
+    TFN_ERR_INVALID_ARGUMENT = 1, /* null pointer, batch < 0, H or W <= 0, overflow, overlap, bad enum */
+    TFN_ERR_CONFIG = 2,           /* fx, fy not finite or <= 0; disparity with fx != fy or bad baseline*f */
+    TFN_ERR_CUDA = 3              /* CUDA launch/runtime error, or the device is not sm_100 */
+} tfn_status;
+
+typedef enum { TFN_FILTER_FD = 0, TFN_FILTER_SOBEL = 1, TFN_FILTER_SCHARR = 2, TFN_FILTER_PREWITT = 3 } tfn_filter;
+typedef enum { TFN_NZ_MEAN = 0, TFN_NZ_MEDIAN = 1 } tfn_nz_mode;
+typedef enum { TFN_LAYOUT_PLANAR = 0, TFN_LAYOUT_PACKED = 1 } tfn_layout;
+
+/* Options for tfn_set_option (tuning / testing; defaults are the production path) */
+typedef enum {
+    TFN_OPT_KERNEL = 0,     /* 0 auto, 1 per-pixel kernel, 2 strip kernel (needs W%4==0, 16-B alignment) */
+    TFN_OPT_STRIP_H = 1,    /* rows per warp strip, 0 = auto (>= 4)                                        */
+    TFN_OPT_GRID = 2,       /* CTAs of the strip kernel, 0 = auto (resident CTAs x SMs)                    */
+    TFN_OPT_STREAMING = 3   /* 1 (default): streaming (evict-first) stores of the normals                  */
+} tfn_option;
+
+/* Pinhole intrinsics in pixels (Eq. 13): u = column, v = row, 0-based, pixel
+ * centres at integer coordinates. */
+typedef struct { double fx, fy, u0, v0; } tfn_intrinsics;
+
+typedef struct tfn_ctx* tfn_handle;
+
+/* Create an estimator for intrinsics K, gradient kernel `filter` (tfn_filter) and
+ * n_z filter `nz_mode` (tfn_nz_mode).  Checks that the current device is sm_100.
+ * Errors: K or out NULL, bad enum -> INVALID_ARGUMENT; fx/fy/u0/v0 non-finite or
+ * fx, fy <= 0 -> CONFIG; no CUDA device / not sm_100 -> CUDA. */
+int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_handle* out);
+
+/* Output layout (tfn_layout); default PLANAR. */
+int tfn_set_layout(tfn_handle h, int layout);
+
+/* Tuning/testing option (tfn_option). */
+int tfn_set_option(tfn_handle h, int option, long long value);
+
+/* 3F2N from depth (Eq. 13-18).  depth: device fp32 [batch,H,W] in metres
+ * (any positive unit); out_normals: device fp32, 3*batch*H*W floats in the
+ * handle's layout.  Asynchronous on stream. */
+int tfn_estimate(tfn_handle h, const float* depth, int batch, int H, int W,
+                 void* stream, float* out_normals);
+
+/* 3F2N from disparity (Eq. 19-21): z = f t_c / d.  Requires fx == fy
+ * (CONFIG otherwise).  baseline_times_f = f * t_c > 0 and finite (CONFIG otherwise);
+ * it cancels from the normal direction and is only validated. */
+int tfn_estimate_disparity(tfn_handle h, const float* disparity, double baseline_times_f,
+                           int batch, int H, int W, void* stream, float* out_normals);
+
+/* End-to-end from HOST memory: copies host_in (fp32 [batch,H,W], depth or
+ * disparity) to the device in chunks, runs the same kernel, copies the normals back
+ * to host_out (3*batch*H*W floats), overlapping H2D / kernel / D2H on two internal
+ * streams.  Pinned host memory gives full overlap.  Blocking: returns when host_out
+ * is complete (or on the first error).  `stream` orders the work after prior work
+ * on that stream. */
+int tfn_estimate_host(tfn_handle h, const float* host_in, int is_disparity, double baseline_times_f,
+                      int batch, int H, int W, float* host_out, void* stream);
+
+/* angular-error statistics (Eq. 22-24) of est (device,
+ * layout `layout`) against gt (device, planar [batch,3,H,W], NaN = invalid), ADDED
+ * into stats_dev (device int64[8]): [0] sum of psi in 1e-6 degree units, [1] m =
+ * pixels valid in both, [2..4] count psi <= 10/20/30 deg, [5] valid estimates,
+ * [6] valid GT, [7] pixels.  psi = atan2(|a x b|, a.b) in fp64. */
+int tfn_stats(const float* est, const float* gt, int batch, int H, int W, int layout,
+              void* stream, long long* stats_dev);
+
+/* Probe of the device Phi (P8): for n groups of 8 candidates (device fp32 [n,8];
+ * a non-finite candidate is skipped) writes Phi (mean or median of the finite ones)
+ * to out_dev[n] and their count to k_dev[n], through the kernel's own code path. */
+int tfn_debug_phi8(const float* cand_dev, long long n, int nz_mode, float* out_dev, int* k_dev,
+                   void* stream);
+
+/* Release a handle (and its workspace).  NULL is OK. */
+int tfn_destroy(tfn_handle h);
+
+/* Static string for a status code. */
+const char* tfn_status_string(int status);
+
+/* Number of kernels this library has launched in the process (for bench accounting). */
+unsigned long long tfn_kernel_launches(void);
+
+/* ABI version (major*10000 + minor*100 + patch). */
+int tfn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TFN_H */

@@ -1,0 +1,320 @@
+// tfn_abi.cu — the C ABI declared in include/tfn.h: argument validation, kernel
+// selection, launch-geometry, the pipelined host-buffer path, status strings.
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include <cuda_runtime.h>
+
+#include "../../include/tfn.h"
+#include "tfn_kernels.h"
+
+#define TFN_API extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+std::atomic<unsigned long long> g_launches{0};
+
+struct Workspace {
+    float* in[2] = {nullptr, nullptr};
+    float* out[2] = {nullptr, nullptr};
+    size_t frames = 0;        // capacity in frames of one chunk
+    size_t frame_px = 0;
+    cudaStream_t s[2] = {nullptr, nullptr};
+    cudaEvent_t start = nullptr;
+};
+
+}  // namespace
+
+struct tfn_ctx {
+    tfn_intrinsics K;
+    int filter;
+    int mode;
+    int layout = TFN_LAYOUT_PLANAR;
+    int kernel = tfn::TFN_KERNEL_AUTO;
+    int strip_h = 0;
+    int grid = 0;
+    int streaming = 1;
+    int device = 0;
+    int sms = 148;
+    int strip_ctas_per_sm[2] = {0, 0};   // depth, disparity
+    std::mutex ws_mu;
+    Workspace ws;
+};
+
+namespace {
+
+bool is_fin(double x) { return std::isfinite(x); }
+
+int check_device(int* dev, int* sms) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); return TFN_ERR_CUDA; }
+    int major = 0, minor = 0, n = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, d) != cudaSuccess ||
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) {
+        cudaGetLastError();
+        return TFN_ERR_CUDA;
+    }
+    if (major != 10 || minor != 0) return TFN_ERR_CUDA;   // built for sm_100a only
+    *dev = d;
+    *sms = n;
+    return TFN_OK;
+}
+
+bool overlap(const void* a, size_t na, const void* b, size_t nb) {
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+}
+
+int validate(tfn_handle h, const float* in, int batch, int H, int W, const float* out) {
+    if (!h) return TFN_ERR_INVALID_ARGUMENT;
+    if (batch < 0 || H <= 0 || W <= 0) return TFN_ERR_INVALID_ARGUMENT;
+    if (batch == 0) return TFN_OK;
+    if (!in || !out) return TFN_ERR_INVALID_ARGUMENT;
+    const unsigned long long px = (unsigned long long)batch * (unsigned long long)H * (unsigned long long)W;
+    if (px > (1ull << 60) / 12) return TFN_ERR_INVALID_ARGUMENT;
+    if (((uintptr_t)in & 3) || ((uintptr_t)out & 3)) return TFN_ERR_INVALID_ARGUMENT;
+    if (overlap(in, px * 4, out, px * 12)) return TFN_ERR_INVALID_ARGUMENT;
+    return TFN_OK;
+}
+
+int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaStream_t st, float* out) {
+    tfn::KernelArgs a;
+    a.in = in;
+    a.out = out;
+    a.B = batch;
+    a.H = H;
+    a.W = W;
+    a.fx = (float)h->K.fx;
+    a.fy = (float)h->K.fy;
+    a.u0 = h->K.u0;
+    a.v0 = h->K.v0;
+    a.layout = h->layout;
+    a.streaming = h->streaming;
+    const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & 15) == 0) && (((uintptr_t)out & 15) == 0);
+    int kernel = h->kernel;
+    if (kernel == tfn::TFN_KERNEL_AUTO) kernel = strip_ok ? tfn::TFN_KERNEL_STRIP : tfn::TFN_KERNEL_PIXEL;
+    if (kernel == tfn::TFN_KERNEL_STRIP && !strip_ok) return TFN_ERR_INVALID_ARGUMENT;
+    int grid = 0;
+    if (kernel == tfn::TFN_KERNEL_STRIP) {
+        const long long resident_warps =
+            (long long)h->sms * h->strip_ctas_per_sm[disp] * (TFN_STRIP_THREADS / 32);
+        int sh = h->strip_h;
+        const long long sx_n = (W + 127) / 128;
+        if (sh <= 0) {
+            // 32 rows per strip amortises the 2 halo rows; shrink it when the batch is
+            // too small to give every resident warp a few strips
+            sh = 32;
+            while (sh > 4 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 2 * resident_warps) sh >>= 1;
+        }
+        a.strip_h = sh;
+        const long long items = sx_n * ((H + sh - 1) / sh) * (long long)batch;
+        long long ctas = h->grid > 0 ? h->grid : (long long)h->sms * h->strip_ctas_per_sm[disp];
+        const long long need = (items + (TFN_STRIP_THREADS / 32) - 1) / (TFN_STRIP_THREADS / 32);
+        if (ctas > need) ctas = need;
+        if (ctas < 1) ctas = 1;
+        grid = (int)ctas;
+    } else {
+        a.strip_h = 0;
+    }
+    cudaError_t e = tfn::launch_3f2n(a, h->filter, h->mode, disp, kernel, grid, st);
+    if (e != cudaSuccess) return TFN_ERR_CUDA;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return TFN_OK;
+}
+
+}  // namespace
+
+
+TFN_API int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_handle* out) {
+    if (!K || !out) return TFN_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    if (filter < 0 || filter > 3 || nz_mode < 0 || nz_mode > 1) return TFN_ERR_INVALID_ARGUMENT;
+    if (!is_fin(K->fx) || !is_fin(K->fy) || !is_fin(K->u0) || !is_fin(K->v0) || K->fx <= 0 || K->fy <= 0)
+        return TFN_ERR_CONFIG;
+    int dev = 0, sms = 0;
+    const int st = check_device(&dev, &sms);
+    if (st != TFN_OK) return st;
+    tfn_ctx* h = new (std::nothrow) tfn_ctx();
+    if (!h) return TFN_ERR_CUDA;
+    h->K = *K;
+    h->filter = filter;
+    h->mode = nz_mode;
+    h->device = dev;
+    h->sms = sms;
+    for (int d = 0; d < 2; ++d) {
+        h->strip_ctas_per_sm[d] = tfn::strip_occupancy(filter, nz_mode, d != 0);
+        if (h->strip_ctas_per_sm[d] <= 0) h->strip_ctas_per_sm[d] = 1;
+    }
+    *out = h;
+    return TFN_OK;
+}
+
+TFN_API int tfn_set_layout(tfn_handle h, int layout) {
+    if (!h || (layout != TFN_LAYOUT_PLANAR && layout != TFN_LAYOUT_PACKED)) return TFN_ERR_INVALID_ARGUMENT;
+    h->layout = layout;
+    return TFN_OK;
+}
+
+TFN_API int tfn_set_option(tfn_handle h, int option, long long value) {
+    if (!h) return TFN_ERR_INVALID_ARGUMENT;
+    switch (option) {
+    case TFN_OPT_KERNEL:
+        if (value < 0 || value > 2) return TFN_ERR_INVALID_ARGUMENT;
+        h->kernel = (int)value;
+        return TFN_OK;
+    case TFN_OPT_STRIP_H:
+        if (value < 0 || value > 1 << 20) return TFN_ERR_INVALID_ARGUMENT;
+        h->strip_h = (int)value;
+        return TFN_OK;
+    case TFN_OPT_GRID:
+        if (value < 0 || value > 1 << 24) return TFN_ERR_INVALID_ARGUMENT;
+        h->grid = (int)value;
+        return TFN_OK;
+    case TFN_OPT_STREAMING:
+        h->streaming = value ? 1 : 0;
+        return TFN_OK;
+    default:
+        return TFN_ERR_INVALID_ARGUMENT;
+    }
+}
+
+TFN_API int tfn_estimate(tfn_handle h, const float* depth, int batch, int H, int W, void* stream,
+                         float* out_normals) {
+    int st = validate(h, depth, batch, H, W, out_normals);
+    if (st != TFN_OK || batch == 0) return st;
+    return run(h, depth, false, batch, H, W, (cudaStream_t)stream, out_normals);
+}
+
+TFN_API int tfn_estimate_disparity(tfn_handle h, const float* disparity, double baseline_times_f,
+                                   int batch, int H, int W, void* stream, float* out_normals) {
+    if (!h) return TFN_ERR_INVALID_ARGUMENT;
+    if (h->K.fx != h->K.fy) return TFN_ERR_CONFIG;                       // Eq. 19: one f
+    if (!is_fin(baseline_times_f) || baseline_times_f <= 0) return TFN_ERR_CONFIG;
+    int st = validate(h, disparity, batch, H, W, out_normals);
+    if (st != TFN_OK || batch == 0) return st;
+    return run(h, disparity, true, batch, H, W, (cudaStream_t)stream, out_normals);
+}
+
+TFN_API int tfn_estimate_host(tfn_handle h, const float* host_in, int is_disparity, double baseline_times_f,
+                              int batch, int H, int W, float* host_out, void* stream) {
+    if (!h) return TFN_ERR_INVALID_ARGUMENT;
+    if (is_disparity) {
+        if (h->K.fx != h->K.fy) return TFN_ERR_CONFIG;
+        if (!is_fin(baseline_times_f) || baseline_times_f <= 0) return TFN_ERR_CONFIG;
+    }
+    if (batch < 0 || H <= 0 || W <= 0) return TFN_ERR_INVALID_ARGUMENT;
+    if (batch == 0) return TFN_OK;
+    if (!host_in || !host_out) return TFN_ERR_INVALID_ARGUMENT;
+    const size_t fpx = (size_t)H * (size_t)W;
+    if ((unsigned long long)batch * fpx > (1ull << 60) / 12) return TFN_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lock(h->ws_mu);
+    Workspace& ws = h->ws;
+    // ~48 MB of input per chunk: large enough to saturate PCIe, small enough to pipeline
+    size_t chunk = (48u << 20) / (fpx * 4);
+    if (chunk < 1) chunk = 1;
+    if (chunk > (size_t)batch) chunk = batch;
+    if (ws.frames < chunk || ws.frame_px != fpx) {
+        for (int i = 0; i < 2; ++i) {
+            if (ws.in[i]) cudaFree(ws.in[i]);
+            if (ws.out[i]) cudaFree(ws.out[i]);
+            ws.in[i] = ws.out[i] = nullptr;
+        }
+        ws.frames = 0;
+        for (int i = 0; i < 2; ++i) {
+            if (cudaMalloc(&ws.in[i], chunk * fpx * 4) != cudaSuccess ||
+                cudaMalloc(&ws.out[i], chunk * fpx * 12) != cudaSuccess) {
+                cudaGetLastError();
+                return TFN_ERR_CUDA;
+            }
+        }
+        ws.frames = chunk;
+        ws.frame_px = fpx;
+    }
+    if (!ws.s[0]) {
+        for (int i = 0; i < 2; ++i)
+            if (cudaStreamCreateWithFlags(&ws.s[i], cudaStreamNonBlocking) != cudaSuccess) return TFN_ERR_CUDA;
+        if (cudaEventCreateWithFlags(&ws.start, cudaEventDisableTiming) != cudaSuccess) return TFN_ERR_CUDA;
+    }
+    cudaStream_t user = (cudaStream_t)stream;
+    if (cudaEventRecord(ws.start, user) != cudaSuccess) return TFN_ERR_CUDA;
+    for (int i = 0; i < 2; ++i)
+        if (cudaStreamWaitEvent(ws.s[i], ws.start, 0) != cudaSuccess) return TFN_ERR_CUDA;
+    int rc = TFN_OK;
+    size_t done = 0;
+    int k = 0;
+    while (done < (size_t)batch) {
+        const size_t n = ((size_t)batch - done < chunk) ? (size_t)batch - done : chunk;
+        cudaStream_t s = ws.s[k & 1];
+        if (cudaMemcpyAsync(ws.in[k & 1], host_in + done * fpx, n * fpx * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+            rc = TFN_ERR_CUDA;
+            break;
+        }
+        rc = run(h, ws.in[k & 1], is_disparity != 0, (int)n, H, W, s, ws.out[k & 1]);
+        if (rc != TFN_OK) break;
+        if (cudaMemcpyAsync(host_out + done * fpx * 3, ws.out[k & 1], n * fpx * 12, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+            rc = TFN_ERR_CUDA;
+            break;
+        }
+        done += n;
+        ++k;
+    }
+    for (int i = 0; i < 2; ++i)
+        if (cudaStreamSynchronize(ws.s[i]) != cudaSuccess) rc = TFN_ERR_CUDA;
+    return rc;
+}
+
+TFN_API int tfn_stats(const float* est, const float* gt, int batch, int H, int W, int layout, void* stream,
+                      long long* stats_dev) {
+    if (batch < 0 || H <= 0 || W <= 0 || (layout != 0 && layout != 1)) return TFN_ERR_INVALID_ARGUMENT;
+    if (batch == 0) return TFN_OK;
+    if (!est || !gt || !stats_dev) return TFN_ERR_INVALID_ARGUMENT;
+    if (tfn::launch_stats(est, gt, batch, H, W, layout, stats_dev, (cudaStream_t)stream) != cudaSuccess)
+        return TFN_ERR_CUDA;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return TFN_OK;
+}
+
+TFN_API int tfn_debug_phi8(const float* cand_dev, long long n, int nz_mode, float* out_dev, int* k_dev,
+                           void* stream) {
+    if (n < 0 || nz_mode < 0 || nz_mode > 1) return TFN_ERR_INVALID_ARGUMENT;
+    if (n == 0) return TFN_OK;
+    if (!cand_dev || !out_dev || !k_dev) return TFN_ERR_INVALID_ARGUMENT;
+    if (tfn::launch_phi8(cand_dev, n, nz_mode, out_dev, k_dev, (cudaStream_t)stream) != cudaSuccess)
+        return TFN_ERR_CUDA;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return TFN_OK;
+}
+
+TFN_API int tfn_destroy(tfn_handle h) {
+    if (!h) return TFN_OK;
+    {
+        std::lock_guard<std::mutex> lock(h->ws_mu);
+        for (int i = 0; i < 2; ++i) {
+            if (h->ws.in[i]) cudaFree(h->ws.in[i]);
+            if (h->ws.out[i]) cudaFree(h->ws.out[i]);
+            if (h->ws.s[i]) cudaStreamDestroy(h->ws.s[i]);
+        }
+        if (h->ws.start) cudaEventDestroy(h->ws.start);
+    }
+    delete h;
+    return TFN_OK;
+}
+
+TFN_API const char* tfn_status_string(int status) {
+    switch (status) {
+    case TFN_OK: return "TFN_OK";
+    case TFN_ERR_INVALID_ARGUMENT: return "TFN_ERR_INVALID_ARGUMENT";
+    case TFN_ERR_CONFIG: return "TFN_ERR_CONFIG";
+    case TFN_ERR_CUDA: return "TFN_ERR_CUDA";
+    default: return "TFN_UNKNOWN_STATUS";
+    }
+}
+
+TFN_API unsigned long long tfn_kernel_launches(void) { return g_launches.load(); }
+
+TFN_API int tfn_version(void) { return 100; }

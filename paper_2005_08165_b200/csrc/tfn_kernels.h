@@ -1,0 +1,38 @@
+// tfn_kernels.h — internal launch interface between the C ABI (tfn_abi.cu) and the
+// kernels (tfn_kernels.cu, tfn_stats.cu).  Not part of the public ABI (include/tfn.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#define TFN_STRIP_THREADS 256
+
+namespace tfn {
+
+enum KernelId { TFN_KERNEL_AUTO = 0, TFN_KERNEL_PIXEL = 1, TFN_KERNEL_STRIP = 2 };
+
+struct KernelArgs {
+    const float* in;     // [B,H,W] depth or disparity
+    float* out;          // [B,3,H,W] (layout 0) or [B,H,W,3] (layout 1)
+    long long B;
+    int H, W;
+    float fx, fy;        // n' = (fx g_u, fy g_v, n_z)   (Eq. 18)
+    double u0, v0;       // a = u - u0, b = v - v0       (Eq. 13)
+    int layout;
+    int strip_h;         // rows per warp strip (strip kernel)
+    int streaming;       // 1: st.global.cs for the normals
+};
+
+cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, int kernel,
+                        int grid_strip, cudaStream_t st);
+
+// resident CTAs per SM of the strip kernel variant (occupancy query)
+int strip_occupancy(int filter, int mode, bool disp);
+
+// a8: angular-error statistics vs ground truth (off the timed path)
+cudaError_t launch_stats(const float* est, const float* gt, long long B, int H, int W,
+                         int layout, long long* stats_dev, cudaStream_t st);
+
+// P8 probe: Phi of n groups of 8 candidates (non-finite = skipped)
+cudaError_t launch_phi8(const float* cand, long long n, int mode, float* out, int* k_out,
+                        cudaStream_t st);
+
+}  // namespace tfn

@@ -1,0 +1,264 @@
+"""Thin ctypes binding of libtfn.so (include/tfn.h) — argument marshalling only.
+
+Every step of the 3F2N path runs in the CUDA kernels behind the C ABI; this
+module never computes normals itself and has no CPU fallback: if libtfn.so is
+missing or the device is not sm_100 the calls raise.  PyTorch is used only for
+device memory and streams.
+
+Functions with the ABI's names (tfn_create, tfn_estimate, ...) take raw pointers
+exactly like the C calls; `Estimator`, `stats` and `debug_phi8` wrap them for
+torch tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence, Tuple
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtfn.so")
+
+TFN_OK, TFN_ERR_INVALID_ARGUMENT, TFN_ERR_CONFIG, TFN_ERR_CUDA = 0, 1, 2, 3
+FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3}
+MODES = {"mean": 0, "median": 1}
+LAYOUTS = {"planar": 0, "packed": 1}
+KERNELS = {"auto": 0, "pixel": 1, "strip": 2}
+OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_STREAMING = 0, 1, 2, 3
+
+# every symbol include/tfn.h declares (tests/test_abi.py checks the export table)
+ABI_SYMBOLS = (
+    "tfn_create", "tfn_set_layout", "tfn_set_option", "tfn_estimate", "tfn_estimate_disparity",
+    "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8", "tfn_destroy", "tfn_status_string",
+    "tfn_kernel_launches", "tfn_version",
+)
+
+
+class TfnError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        super().__init__(f"{where}: {tfn_status_string(status)} ({status})")
+
+
+class tfn_intrinsics(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_double), ("fy", ctypes.c_double),
+                ("u0", ctypes.c_double), ("v0", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libtfn.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built — run `python -m paper_2005_08165_b200.build` "
+                              "(the 3F2N path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i, d, ll = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_longlong
+        L.tfn_create.argtypes = [ctypes.POINTER(tfn_intrinsics), i, i, ctypes.POINTER(vp)]
+        L.tfn_set_layout.argtypes = [vp, i]
+        L.tfn_set_option.argtypes = [vp, i, ll]
+        L.tfn_estimate.argtypes = [vp, vp, i, i, i, vp, vp]
+        L.tfn_estimate_disparity.argtypes = [vp, vp, d, i, i, i, vp, vp]
+        L.tfn_estimate_host.argtypes = [vp, vp, i, d, i, i, i, vp, vp]
+        L.tfn_stats.argtypes = [vp, vp, i, i, i, i, vp, vp]
+        L.tfn_debug_phi8.argtypes = [vp, ll, i, vp, vp, vp]
+        L.tfn_destroy.argtypes = [vp]
+        L.tfn_status_string.argtypes = [i]
+        L.tfn_status_string.restype = ctypes.c_char_p
+        L.tfn_kernel_launches.restype = ctypes.c_ulonglong
+        for name in ABI_SYMBOLS:
+            f = getattr(L, name)
+            if f.restype is ctypes.c_int or name in ("tfn_create", "tfn_set_layout", "tfn_set_option",
+                                                     "tfn_estimate", "tfn_estimate_disparity",
+                                                     "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8",
+                                                     "tfn_destroy", "tfn_version"):
+                f.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+# ----------------------------------------------------------------- ABI-named calls
+def tfn_status_string(status: int) -> str:
+    try:
+        return lib().tfn_status_string(int(status)).decode()
+    except ImportError:
+        return str(status)
+
+
+def _check(rc: int, where: str):
+    if rc != TFN_OK:
+        raise TfnError(rc, where)
+
+
+def tfn_create(K, filter: int, nz_mode: int) -> int:
+    fx, fy, u0, v0 = K.as_tuple() if hasattr(K, "as_tuple") else tuple(K)
+    k = tfn_intrinsics(float(fx), float(fy), float(u0), float(v0))
+    h = ctypes.c_void_p()
+    _check(lib().tfn_create(ctypes.byref(k), int(filter), int(nz_mode), ctypes.byref(h)), "tfn_create")
+    return h.value
+
+
+def tfn_set_layout(h: int, layout: int) -> None:
+    _check(lib().tfn_set_layout(h, int(layout)), "tfn_set_layout")
+
+
+def tfn_set_option(h: int, option: int, value: int) -> None:
+    _check(lib().tfn_set_option(h, int(option), int(value)), "tfn_set_option")
+
+
+def tfn_estimate(h: int, depth_ptr: int, batch: int, H: int, W: int, stream: int, out_ptr: int) -> int:
+    return lib().tfn_estimate(h, depth_ptr, batch, H, W, stream, out_ptr)
+
+
+def tfn_estimate_disparity(h: int, disp_ptr: int, baseline_times_f: float, batch: int, H: int, W: int,
+                           stream: int, out_ptr: int) -> int:
+    return lib().tfn_estimate_disparity(h, disp_ptr, float(baseline_times_f), batch, H, W, stream, out_ptr)
+
+
+def tfn_estimate_host(h: int, host_in: int, is_disparity: int, baseline_times_f: float, batch: int,
+                      H: int, W: int, host_out: int, stream: int) -> int:
+    return lib().tfn_estimate_host(h, host_in, int(is_disparity), float(baseline_times_f), batch, H, W,
+                                   host_out, stream)
+
+
+def tfn_stats(est_ptr: int, gt_ptr: int, batch: int, H: int, W: int, layout: int, stream: int,
+              stats_ptr: int) -> int:
+    return lib().tfn_stats(est_ptr, gt_ptr, batch, H, W, layout, stream, stats_ptr)
+
+
+def tfn_debug_phi8(cand_ptr: int, n: int, nz_mode: int, out_ptr: int, k_ptr: int, stream: int) -> int:
+    return lib().tfn_debug_phi8(cand_ptr, n, nz_mode, out_ptr, k_ptr, stream)
+
+
+def tfn_destroy(h: int) -> int:
+    return lib().tfn_destroy(h)
+
+
+def tfn_kernel_launches() -> int:
+    return int(lib().tfn_kernel_launches())
+
+
+def tfn_version() -> int:
+    return int(lib().tfn_version())
+
+
+# ----------------------------------------------------------------- tensor helpers
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _need(t: torch.Tensor, name: str, device: bool = True):
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        raise TfnError(TFN_ERR_INVALID_ARGUMENT, f"{name} must be a contiguous float32 tensor")
+    if device and not t.is_cuda:
+        raise TfnError(TFN_ERR_INVALID_ARGUMENT, f"{name} must be a CUDA tensor")
+
+
+def _bhw(x: torch.Tensor) -> Tuple[int, int, int]:
+    if x.dim() == 2:
+        return 1, x.shape[0], x.shape[1]
+    if x.dim() == 3:
+        return x.shape[0], x.shape[1], x.shape[2]
+    raise TfnError(TFN_ERR_INVALID_ARGUMENT, "input must be [H,W] or [B,H,W]")
+
+
+class Estimator:
+    """One tfn handle: intrinsics K=(fx,fy,u0,v0), gradient kernel, Phi, layout."""
+
+    def __init__(self, K, filter: str = "sobel", nz_mode: str = "median", layout: str = "planar",
+                 kernel: str = "auto", strip_h: int = 0, grid: int = 0, streaming: bool = True):
+        self.K = K.as_tuple() if hasattr(K, "as_tuple") else tuple(float(x) for x in K)
+        self.filter, self.nz_mode, self.layout = filter, nz_mode, layout
+        self.h = tfn_create(self.K, FILTERS[filter], MODES[nz_mode])
+        tfn_set_layout(self.h, LAYOUTS[layout])
+        tfn_set_option(self.h, OPT_KERNEL, KERNELS[kernel])
+        tfn_set_option(self.h, OPT_STRIP_H, strip_h)
+        tfn_set_option(self.h, OPT_GRID, grid)
+        tfn_set_option(self.h, OPT_STREAMING, int(streaming))
+
+    def _out(self, B, H, W, like: torch.Tensor, out):
+        shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float32, device=like.device)
+        _need(out, "out", device=like.is_cuda)
+        if out.numel() != 3 * B * H * W:
+            raise TfnError(TFN_ERR_INVALID_ARGUMENT, "out has the wrong size")
+        return out
+
+    def estimate(self, depth: torch.Tensor, out: Optional[torch.Tensor] = None,
+                 stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        _need(depth, "depth")
+        B, H, W = _bhw(depth)
+        out = self._out(B, H, W, depth, out)
+        _check(tfn_estimate(self.h, depth.data_ptr(), B, H, W, _stream_ptr(stream), out.data_ptr()),
+               "tfn_estimate")
+        return out
+
+    def estimate_disparity(self, disp: torch.Tensor, baseline_times_f: float,
+                           out: Optional[torch.Tensor] = None,
+                           stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        _need(disp, "disparity")
+        B, H, W = _bhw(disp)
+        out = self._out(B, H, W, disp, out)
+        _check(tfn_estimate_disparity(self.h, disp.data_ptr(), baseline_times_f, B, H, W,
+                                      _stream_ptr(stream), out.data_ptr()), "tfn_estimate_disparity")
+        return out
+
+    def estimate_host(self, host_in: torch.Tensor, is_disparity: bool = False, baseline_times_f: float = 1.0,
+                      out: Optional[torch.Tensor] = None,
+                      stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Host buffers in and out (pinned for full overlap); blocking."""
+        _need(host_in, "host_in", device=False)
+        if host_in.is_cuda:
+            raise TfnError(TFN_ERR_INVALID_ARGUMENT, "host_in must be a CPU tensor")
+        B, H, W = _bhw(host_in)
+        if out is None:
+            shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
+            out = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        _check(tfn_estimate_host(self.h, host_in.data_ptr(), int(is_disparity), baseline_times_f, B, H, W,
+                                 out.data_ptr(), _stream_ptr(stream)), "tfn_estimate_host")
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            tfn_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def stats(est: torch.Tensor, gt: torch.Tensor, layout: str = "planar", acc: Optional[torch.Tensor] = None,
+          stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """Accumulate the a8 statistics of est vs gt into acc (int64[8] on the device)."""
+    _need(est, "est")
+    _need(gt, "gt")
+    B, H, W = gt.shape[0], gt.shape[2], gt.shape[3]
+    if acc is None:
+        acc = torch.zeros(8, dtype=torch.int64, device=est.device)
+    _check(tfn_stats(est.data_ptr(), gt.data_ptr(), B, H, W, LAYOUTS[layout], _stream_ptr(stream),
+                     acc.data_ptr()), "tfn_stats")
+    return acc
+
+
+def debug_phi8(cand: torch.Tensor, nz_mode: str) -> Tuple[torch.Tensor, torch.Tensor]:
+    """P8 probe: device Phi of [n,8] candidates (non-finite = skipped)."""
+    _need(cand, "cand")
+    n = cand.numel() // 8
+    out = torch.empty(n, dtype=torch.float32, device=cand.device)
+    k = torch.empty(n, dtype=torch.int32, device=cand.device)
+    _check(tfn_debug_phi8(cand.data_ptr(), n, MODES[nz_mode], out.data_ptr(), k.data_ptr(),
+                          _stream_ptr(None)), "tfn_debug_phi8")
+    return out, k
+
+
+STAT_KEYS = ("sum_psi_micro_deg", "m", "n_le_10", "n_le_20", "n_le_30", "n_valid_est", "n_valid_gt",
+             "n_pixels")
