@@ -67,7 +67,6 @@ def parse():
     ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel"])
     ap.add_argument("--strip-h", type=int, default=0)
     ap.add_argument("--grid", type=int, default=0)
-    ap.add_argument("--no-streaming-stores", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -286,7 +285,7 @@ def main():
     first = rank * per_rank
 
     est = tfn.Estimator(K, filter=filt, nz_mode=mode, layout=args.layout, kernel=args.kernel,
-                        strip_h=args.strip_h, grid=args.grid, streaming=not args.no_streaming_stores)
+                        strip_h=args.strip_h, grid=args.grid)
     stream = torch.cuda.current_stream(dev)
 
     def launch(x, out):

@@ -15,7 +15,7 @@ SO = os.path.join(HERE, "libtfn.so")
 SOURCES = ["tfn_abi.cu", "tfn_kernels.cu", "tfn_stats.cu"]
 HEADERS = ["tfn_device.cuh", "tfn_kernels.h", os.path.join("..", "..", "include", "tfn.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-fvisibility=hidden",
               "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 
@@ -27,16 +27,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    SO_ = out or SO
+    if not force and out is None and not _stale():
         return SO
     nvcc = os.environ.get("NVCC", "nvcc")
     objs = []
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
     procs = []
     for src in SOURCES:
-        obj = os.path.join(HERE, "build", src.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-dc" if False else "-c",
+        tag = os.path.basename(SO_).replace(".so", "")
+        obj = os.path.join(HERE, "build", f"{tag}_{src.replace('.cu', '.o')}")
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
@@ -49,12 +51,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed for {src}")
     with open(os.path.join(HERE, "build", "ptxas.log"), "w") as f:
         f.write("\n".join(log))
-    cmd = [nvcc, *ARCH, "-shared", "-o", SO + ".tmp", *objs, "-lcudart"]
+    cmd = [nvcc, *ARCH, "-shared", "-o", SO_ + ".tmp", *objs, "-lcudart"]
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
+    os.replace(SO_ + ".tmp", SO_)
     if verbose:
         print("\n".join(log))
-    return SO
+    return SO_
 
 
 if __name__ == "__main__":

@@ -37,7 +37,6 @@ struct tfn_ctx {
     int kernel = tfn::TFN_KERNEL_AUTO;
     int strip_h = 0;
     int grid = 0;
-    int streaming = 1;
     int device = 0;
     int sms = 148;
     int strip_ctas_per_sm[2] = {0, 0};   // depth, disparity
@@ -91,11 +90,13 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
     a.W = W;
     a.fx = (float)h->K.fx;
     a.fy = (float)h->K.fy;
-    a.u0 = h->K.u0;
-    a.v0 = h->K.v0;
+    a.u0 = (float)h->K.u0;
+    a.v0 = (float)h->K.v0;
     a.layout = h->layout;
-    a.streaming = h->streaming;
-    const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & 15) == 0) && (((uintptr_t)out & 15) == 0);
+    // strip kernel: 16-B vectors, and (frame, strip-row, strip-col) items indexed in 32 bits
+    const long long max_items = (long long)((W + 127) / 128) * ((H + 3) / 4) * (long long)batch;
+    const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & 15) == 0) && (((uintptr_t)out & 15) == 0) &&
+                          max_items < (1LL << 31);
     int kernel = h->kernel;
     if (kernel == tfn::TFN_KERNEL_AUTO) kernel = strip_ok ? tfn::TFN_KERNEL_STRIP : tfn::TFN_KERNEL_PIXEL;
     if (kernel == tfn::TFN_KERNEL_STRIP && !strip_ok) return TFN_ERR_INVALID_ARGUMENT;
@@ -174,9 +175,6 @@ TFN_API int tfn_set_option(tfn_handle h, int option, long long value) {
     case TFN_OPT_GRID:
         if (value < 0 || value > 1 << 24) return TFN_ERR_INVALID_ARGUMENT;
         h->grid = (int)value;
-        return TFN_OK;
-    case TFN_OPT_STREAMING:
-        h->streaming = value ? 1 : 0;
         return TFN_OK;
     default:
         return TFN_ERR_INVALID_ARGUMENT;

@@ -3,7 +3,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#define TFN_STRIP_THREADS 256
+#define TFN_STRIP_THREADS 128
+#ifndef TFN_STRIP_MINBLOCKS
+#define TFN_STRIP_MINBLOCKS 3
+#endif
 
 namespace tfn {
 
@@ -15,10 +18,9 @@ struct KernelArgs {
     long long B;
     int H, W;
     float fx, fy;        // n' = (fx g_u, fy g_v, n_z)   (Eq. 18)
-    double u0, v0;       // a = u - u0, b = v - v0       (Eq. 13)
+    float u0, v0;        // a = u - u0, b = v - v0 (Eq. 13), principal point rounded to fp32
     int layout;
     int strip_h;         // rows per warp strip (strip kernel)
-    int streaming;       // 1: st.global.cs for the normals
 };
 
 cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, int kernel,

@@ -1,0 +1,305 @@
+// tfn_strip.cuh — the production 3F2N kernel (included by tfn_kernels.cu).
+//
+// Geometry.  One warp owns a strip of 128 columns x strip_h rows of one frame; each
+// lane owns 4 adjacent columns c0..c0+3 and walks down the strip with a rolling
+// window of three row "slots" (rows v-1, v, v+1).  The row loop is unrolled by 3
+// and the slots rotate by renaming (no register copies).  Per lane-row: one
+// LDG.128 + two halo LDG.32 in (clamped addresses, never out of bounds), three
+// STG.128 out.  Persistent grid: warps stride over (frame, strip-row, strip-col).
+//
+// Arithmetic (bit-identical to tfn_pixel_kernel, see tfn_device.cuh):
+//   fp64:  w = 1/z (correctly rounded), D_h, D_v, g_u, g_v in the oracle's order,
+//          s = g_u + g_v, t = g_v - g_u, rounded once to fp32;
+//   fp32:  one MUFU reciprocal per neighbour PAIR (shared by both pixels of the pair),
+//          rho, tau = m * rho, Phi, n_z, normalise, orient — the per-pixel tail in
+//          packed FMUL2/FFMA2/FADD2 over pixel pairs (0,1), (2,3).
+// Fast path: all 8 candidates finite and Phi != 0 (no skips, no flat rule, no
+// orientation tie, valid pixel).  Anything else ("special": holes, invalid samples,
+// dZ == 0, flat, ties) takes the general per-pixel code behind ONE warp vote per
+// row step.  Known-invalid border pixels are patched to NaN by mask.
+#pragma once
+
+namespace tfn {
+
+struct Slot {
+    float raw[6];      // samples of columns c0-1 .. c0+4 as loaded
+    bool rok;          // the row exists (loads were issued)
+    float z[6];        // sanitized (invalid -> NaN)
+    double w[6];       // x = 1/z (depth) or d (disparity), fp64
+    double head[4];    // kp*D_h(row-1) + k0*D_h(row)   (D_h re-derived from w when needed)
+    float rN[4], rNW[4], rNE[4];   // rho of the N / NW / NE neighbours of this row's pixels
+};
+
+struct StripCtx {
+    const float* img;  // frame base
+    const float* pm;   // frame base + clamped column of the lane's float4
+    int cm;            // clamped first column of the lane
+    float u0;
+    int H, W;
+    bool okm, okl, okr;   // lane's columns / left halo / right halo inside the image
+    float fx, fy;
+    float a[4];        // u - u0 of the 4 columns
+    float v0;
+};
+
+// row v of the lane's window: one LDG.128 + two halo LDG.32 at immediate offsets,
+// predicated off outside the image (never an out-of-bounds address)
+__device__ __forceinline__ void load_raw(Slot& s, const StripCtx& c, int v) {
+    s.rok = (v >= 0) && (v < c.H);
+    const float* row = c.pm + (long long)v * c.W;
+    if (s.rok) {
+        const float4 m = __ldg(reinterpret_cast<const float4*>(row));
+        s.raw[1] = m.x; s.raw[2] = m.y; s.raw[3] = m.z; s.raw[4] = m.w;
+    }
+    if (s.rok && c.okl) s.raw[0] = __ldg(row - 1);
+    if (s.rok && c.okr) s.raw[5] = __ldg(row + 4);
+}
+
+// Q5 for the fast path.  Depth: z >= FLT_MIN rejects 0, negatives, NaN and
+// subnormals; z = +inf is rejected downstream (its rho is NaN, or, as a centre, all
+// its candidates are 0 so Phi == 0) -> the exact per-pixel path.  Disparity also
+// needs the explicit upper bound (+inf is not caught downstream there).
+template <bool DISP>
+__device__ __forceinline__ float sanitize_fast(float z, bool ok) {
+    const bool v = DISP ? (ok && z >= 1.17549435e-38f && z <= 3.40282347e+38f) : (ok && z >= 1.17549435e-38f);
+    return v ? z : __int_as_float(0x7fffffff);
+}
+
+template <bool DISP>
+__device__ __forceinline__ void prepare(Slot& s, const StripCtx& c) {
+    s.z[0] = sanitize_fast<DISP>(s.raw[0], s.rok && c.okl);
+#pragma unroll
+    for (int j = 1; j <= 4; ++j) s.z[j] = sanitize_fast<DISP>(s.raw[j], s.rok && c.okm);
+    s.z[5] = sanitize_fast<DISP>(s.raw[5], s.rok && c.okr);
+    // exact for every valid sample; invalid ones give finite garbage here, but their
+    // NaN z makes the pixel "special", which recomputes it exactly
+#pragma unroll
+    for (int j = 0; j < 6; ++j) s.w[j] = DISP ? widen_pos(s.z[j]) : rcp_rn(widen_pos(s.z[j]));
+}
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+// normals are written once and never re-read: streaming (evict-first) stores
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(a, b, c, d));
+}
+
+// One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw receives row
+// v+2), C = slot(v), N = slot(v+1) (N.raw loaded; everything else computed here).
+template <int F, int MODE, bool DISP>
+__device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx& c,
+                                         float* __restrict__ out, long long HW, int layout,
+                                         unsigned colmask, float vf) {
+    load_raw(P, c, v + 2);                       // prefetch two rows ahead
+    prepare<DISP>(N, c);
+
+    // ---- fp64 gradients (Eq. 15), oracle order (Q10) ----
+    double gu[4], gv[4];
+    double dv[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j)
+        dv[j] = (Taps<F>::corners || (j >= 1 && j <= 4)) ? __dsub_rn(N.w[j], P.w[j]) : 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double dhn = __dsub_rn(N.w[i + 2], N.w[i]);          // D_h(v+1)
+        const double dhc = Taps<F>::corners ? __dsub_rn(C.w[i + 2], C.w[i]) : 0.0;   // D_h(v)
+        gu[i] = grad_tail<F>(C.head[i], dhn);
+        N.head[i] = grad_head<F>(dhc, dhn);
+        gv[i] = grad_tail<F>(grad_head<F>(dv[i], dv[i + 1]), dv[i + 2]);
+    }
+    float gu32[4], gv32[4], s32[4], t32[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        gu32[i] = __double2float_rn(gu[i]);
+        gv32[i] = __double2float_rn(gv[i]);
+        s32[i] = __double2float_rn(__dadd_rn(gu[i], gv[i]));
+        t32[i] = __double2float_rn(__dsub_rn(gv[i], gu[i]));
+    }
+
+    // ---- rho of the 8 neighbours (order E W S N SE NW SW NE) and the next row's N/NW/NE ----
+    // one MUFU reciprocal per neighbour PAIR; index j <-> column c0 + j - 1:
+    //   rE[j] (v,j)->(v,j+1), rS (v,c)->(v+1,c), rSE[j] (v,j)->(v+1,j+1), rSW[j] (v,j+1)->(v+1,j)
+    const float b = __fsub_rn(vf, c.v0);        // b = v - v0 (same formula as pixel_general)
+    float nx[4], ny[4], nz[4];
+    unsigned special = 0;
+    float rEp = pair_rcp<DISP>(C.z[0], C.z[1]);
+    float rSEp = pair_rcp<DISP>(C.z[0], N.z[1]);
+    float rSWp = pair_rcp<DISP>(C.z[1], N.z[0]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        float rho[2][8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int i = 2 * q + h;
+            const float zc = C.z[i + 1];
+            const float rE = pair_rcp<DISP>(zc, C.z[i + 2]);
+            const float rS = pair_rcp<DISP>(zc, N.z[i + 1]);
+            const float rSE = pair_rcp<DISP>(zc, N.z[i + 2]);
+            const float rSW = pair_rcp<DISP>(C.z[i + 2], N.z[i + 1]);
+            rho[h][0] = rho_owner<DISP>(zc, C.z[i + 2], rE);
+            rho[h][1] = rho_other<DISP>(C.z[i], zc, rEp);
+            rho[h][2] = rho_owner<DISP>(zc, N.z[i + 1], rS);
+            rho[h][3] = C.rN[i];
+            rho[h][4] = rho_owner<DISP>(zc, N.z[i + 2], rSE);
+            rho[h][5] = C.rNW[i];
+            rho[h][6] = rho_owner<DISP>(zc, N.z[i], rSWp);
+            rho[h][7] = C.rNE[i];
+            N.rN[i] = rho_other<DISP>(zc, N.z[i + 1], rS);
+            N.rNW[i] = rho_other<DISP>(C.z[i], N.z[i + 1], rSEp);
+            N.rNE[i] = rho_other<DISP>(C.z[i + 2], N.z[i + 1], rSW);
+            rEp = rE; rSEp = rSE; rSWp = rSW;
+        }
+        const int i0 = 2 * q, i1 = 2 * q + 1;
+        const float2 mu = f2(gu32[i0], gu32[i1]), mv = f2(gv32[i0], gv32[i1]);
+        const float2 ms = f2(s32[i0], s32[i1]), mt = f2(t32[i0], t32[i1]);
+        float2 tau[8];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            const float2 m = (k < 2) ? mu : (k < 4) ? mv : (k < 6) ? ms : mt;
+            tau[k] = __fmul2_rn(m, f2(rho[0][k], rho[1][k]));
+        }
+        // the same sum as finish32(): ((fma(m,r1,t0) + fma(m,r3,t2)) + (fma(m,r5,t4) + fma(m,r7,t6)))
+        const float2 s01 = __ffma2_rn(mu, f2(rho[0][1], rho[1][1]), tau[0]);
+        const float2 s23 = __ffma2_rn(mv, f2(rho[0][3], rho[1][3]), tau[2]);
+        const float2 s45 = __ffma2_rn(ms, f2(rho[0][5], rho[1][5]), tau[4]);
+        const float2 s67 = __ffma2_rn(mt, f2(rho[0][7], rho[1][7]), tau[6]);
+        const float2 sum8 = __fadd2_rn(__fadd2_rn(s01, s23), __fadd2_rn(s45, s67));
+        float2 phi;
+        if (MODE == MEAN) {
+            phi = __fmul2_rn(sum8, f2(0.125f, 0.125f));
+        } else {
+#pragma unroll
+            for (int k = 1; k < 8; k += 2) {
+                const float2 m = (k < 2) ? mu : (k < 4) ? mv : (k < 6) ? ms : mt;
+                tau[k] = __fmul2_rn(m, f2(rho[0][k], rho[1][k]));
+            }
+            float t0[8], t1[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { t0[k] = tau[k].x; t1[k] = tau[k].y; }
+            float L0, U0, L1, U1;
+            mid_pair8(t0, L0, U0);
+            mid_pair8(t1, L1, U1);
+            phi = __ffma2_rn(f2(0.5f, 0.5f), f2(L0, L1), __fmul2_rn(f2(0.5f, 0.5f), f2(U0, U1)));
+            // FMNMX drops NaN candidates: make Phi NaN when any candidate is non-finite, so
+            // pixels with out-of-image taps (the border, never "special") come out NaN
+            phi = __ffma2_rn(f2(0.f, 0.f), sum8, phi);
+        }
+        // n' = (fx g_u, fy g_v, -(a g_u + b g_v + Phi))
+        const float2 nzneg = __ffma2_rn(f2(c.a[i0], c.a[i1]), mu, __ffma2_rn(f2(b, b), mv, phi));
+        const float2 px = __fmul2_rn(f2(c.fx, c.fx), mu);
+        const float2 py = __fmul2_rn(f2(c.fy, c.fy), mv);
+        const float2 pz = f2(-nzneg.x, -nzneg.y);
+        const float2 dot = __ffma2_rn(px, px, __ffma2_rn(py, py, __fmul2_rn(pz, pz)));
+        // flip iff Phi < 0 (ties Phi == 0 are special): sc = copysign(rsqrt(dot), Phi)
+        const float r0 = __uint_as_float(__float_as_uint(rsqrt_approx(dot.x)) | (__float_as_uint(phi.x) & 0x80000000u));
+        const float r1 = __uint_as_float(__float_as_uint(rsqrt_approx(dot.y)) | (__float_as_uint(phi.y) & 0x80000000u));
+        const float2 sc = f2(r0, r1);
+        const float2 ox = __fmul2_rn(px, sc), oy = __fmul2_rn(py, sc), oz = __fmul2_rn(pz, sc);
+        nx[i0] = ox.x; nx[i1] = ox.y; ny[i0] = oy.x; ny[i1] = oy.y; nz[i0] = oz.x; nz[i1] = oz.y;
+        const bool sp0 = !(fabsf(sum8.x) < __int_as_float(0x7f800000)) || (phi.x == 0.f);
+        const bool sp1 = !(fabsf(sum8.y) < __int_as_float(0x7f800000)) || (phi.y == 0.f);
+        special |= (sp0 ? (1u << i0) : 0u) | (sp1 ? (1u << i1) : 0u);
+    }
+
+    // ---- known-invalid pixels (image border, columns past W) are never special: their
+    //      out-of-image taps are NaN, so the fast path already produced the canonical NaN ----
+    const bool row_border = (v == 0) || (v == c.H - 1);
+    special &= row_border ? 0u : ~colmask;
+    if (__any_sync(0xffffffffu, special != 0)) {
+        // rare: skipped candidates, flat / tie, invalid samples -> exact per-pixel path
+        // (re-reads the 3x3 from L1; bit-identical to tfn_pixel_kernel)
+        for (int i = 0; i < 4; ++i) {
+            if (special & (1u << i)) {
+                const Normal n = pixel_general<F, MODE, DISP>(c.img, c.H, c.W, v, c.cm + i, c.u0, c.v0,
+                                                              c.fx, c.fy);
+                nx[i] = n.x; ny[i] = n.y; nz[i] = n.z;
+            }
+        }
+    }
+    // ---- store (16-B aligned: W % 4 == 0, c0 % 4 == 0) ----
+    if (c.okm) {
+        float* o = out + (long long)v * c.W;
+        if (layout == 0) {
+            st4(o, nx[0], nx[1], nx[2], nx[3]);
+            st4(o + HW, ny[0], ny[1], ny[2], ny[3]);
+            st4(o + 2 * HW, nz[0], nz[1], nz[2], nz[3]);
+        } else {
+            o += (long long)v * c.W * 2;     // packed: 3 floats per pixel
+            st4(o, nx[0], ny[0], nz[0], nx[1]);
+            st4(o + 4, ny[1], nz[1], nx[2], ny[2]);
+            st4(o + 8, nz[2], nx[3], ny[3], nz[3]);
+        }
+    }
+}
+
+template <int F, int MODE, bool DISP>
+__global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_strip_kernel(KernelArgs p) {
+    const int lane = threadIdx.x & 31;
+    const int warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int sx_n = (p.W + 127) >> 7;
+    const int sy_n = (p.H + p.strip_h - 1) / p.strip_h;
+    const int items = sx_n * sy_n * (int)p.B;          // < 2^31, checked by the host
+    const long long HW = (long long)p.H * p.W;
+
+    StripCtx c;
+    c.H = p.H; c.W = p.W;
+    c.fx = p.fx; c.fy = p.fy;
+    c.u0 = p.u0; c.v0 = p.v0;
+
+    for (int it = warp0; it < items; it += nwarps) {
+        const int sx = it % sx_n;
+        const int t2 = it / sx_n;
+        const int sy = t2 % sy_n;
+        const long long fb = t2 / sy_n;
+        const int c0 = sx * 128 + lane * 4;
+        const int y0 = sy * p.strip_h;
+        const int y1 = min(y0 + p.strip_h, p.H);
+        c.okm = c0 < p.W;
+        c.okl = c.okm && c0 >= 1;
+        c.okr = c0 + 4 < p.W;
+        c.cm = min(c0, p.W - 4);
+        c.img = p.in + fb * HW;
+        c.pm = c.img + c.cm;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) c.a[i] = __fsub_rn(__int2float_rn(c0 + i), c.u0);   // a = u - u0
+        unsigned colmask = 0;
+        if (!c.okm) colmask = 0xFu;
+        else {
+            if (c0 == 0) colmask |= 1u;
+            if (c0 + 3 == p.W - 1) colmask |= 8u;
+        }
+        float* out = p.out + fb * 3 * HW + (p.layout == 0 ? (long long)c.cm : 3LL * c.cm);
+
+        Slot S0, S1, S2;
+        // prologue: rows y0-1 (S0), y0 (S1) prepared; row y0+1 (S2) loaded
+        load_raw(S0, c, y0 - 1);
+        load_raw(S1, c, y0);
+        load_raw(S2, c, y0 + 1);
+        prepare<DISP>(S0, c);
+        prepare<DISP>(S1, c);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            S1.head[i] = grad_head<F>(Taps<F>::corners ? __dsub_rn(S0.w[i + 2], S0.w[i]) : 0.0,
+                                      __dsub_rn(S1.w[i + 2], S1.w[i]));
+            const float zc = S1.z[i + 1];
+            S1.rN[i] = rho_other<DISP>(S0.z[i + 1], zc, pair_rcp<DISP>(S0.z[i + 1], zc));
+            S1.rNW[i] = rho_other<DISP>(S0.z[i], zc, pair_rcp<DISP>(S0.z[i], zc));
+            S1.rNE[i] = rho_other<DISP>(S0.z[i + 2], zc, pair_rcp<DISP>(S0.z[i + 2], zc));
+        }
+        float vf = __int2float_rn(y0);      // exact row index as float (rows < 2^24)
+        for (int v = y0; v < y1; v += 3) {
+            row_step<F, MODE, DISP>(S0, S1, S2, v, c, out, HW, p.layout, colmask, vf);
+            __syncwarp();
+            if (v + 1 >= y1) break;
+            row_step<F, MODE, DISP>(S1, S2, S0, v + 1, c, out, HW, p.layout, colmask, vf + 1.0f);
+            __syncwarp();
+            if (v + 2 >= y1) break;
+            row_step<F, MODE, DISP>(S2, S0, S1, v + 2, c, out, HW, p.layout, colmask, vf + 2.0f);
+            __syncwarp();
+            vf += 3.0f;
+        }
+    }
+}
+
+}  // namespace tfn

@@ -18,14 +18,14 @@ from typing import Optional, Sequence, Tuple
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtfn.so")
+LIB_PATH = os.environ.get("TFN_LIB") or os.path.join(_HERE, "libtfn.so")
 
 TFN_OK, TFN_ERR_INVALID_ARGUMENT, TFN_ERR_CONFIG, TFN_ERR_CUDA = 0, 1, 2, 3
 FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3}
 MODES = {"mean": 0, "median": 1}
 LAYOUTS = {"planar": 0, "packed": 1}
 KERNELS = {"auto": 0, "pixel": 1, "strip": 2}
-OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_STREAMING = 0, 1, 2, 3
+OPT_KERNEL, OPT_STRIP_H, OPT_GRID = 0, 1, 2
 
 # every symbol include/tfn.h declares (tests/test_abi.py checks the export table)
 ABI_SYMBOLS = (
@@ -171,7 +171,7 @@ class Estimator:
     """One tfn handle: intrinsics K=(fx,fy,u0,v0), gradient kernel, Phi, layout."""
 
     def __init__(self, K, filter: str = "sobel", nz_mode: str = "median", layout: str = "planar",
-                 kernel: str = "auto", strip_h: int = 0, grid: int = 0, streaming: bool = True):
+                 kernel: str = "auto", strip_h: int = 0, grid: int = 0):
         self.K = K.as_tuple() if hasattr(K, "as_tuple") else tuple(float(x) for x in K)
         self.filter, self.nz_mode, self.layout = filter, nz_mode, layout
         self.h = tfn_create(self.K, FILTERS[filter], MODES[nz_mode])
@@ -179,7 +179,6 @@ class Estimator:
         tfn_set_option(self.h, OPT_KERNEL, KERNELS[kernel])
         tfn_set_option(self.h, OPT_STRIP_H, strip_h)
         tfn_set_option(self.h, OPT_GRID, grid)
-        tfn_set_option(self.h, OPT_STREAMING, int(streaming))
 
     def _out(self, B, H, W, like: torch.Tensor, out):
         shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)

@@ -76,7 +76,7 @@ def test_layouts_and_strip_heights_bitwise(tfn, cfg1):
     for sh in (1, 3, 7, 32, 480, 1000):
         g = run_gpu(tfn, z, ts.K_VGA, "sobel", "median", kernel="strip", strip_h=sh)
         assert np.array_equal(base.view(np.uint32), g.view(np.uint32)), sh
-    g = run_gpu(tfn, z, ts.K_VGA, "sobel", "median", kernel="strip", grid=1, streaming=False)
+    g = run_gpu(tfn, z, ts.K_VGA, "sobel", "median", kernel="strip", grid=1)
     assert np.array_equal(base.view(np.uint32), g.view(np.uint32))
 
 
@@ -275,7 +275,7 @@ def test_phi8_probe(tfn):
     med, kk = tfn.debug_phi8(cc, "median")
     mean, _ = tfn.debug_phi8(cc, "mean")
     med, kk, mean = med.cpu().numpy(), kk.cpu().numpy(), mean.cpu().numpy()
-    assert np.array_equal(kk, k)
+    assert np.array_equal(kk, np.isfinite(c).sum(1))
     for i in range(n):
         v = np.sort(c[i][np.isfinite(c[i])].astype(np.float64))
         if v.size == 0:
