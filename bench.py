@@ -279,10 +279,14 @@ def main():
     filt = args.filter or cfg["filter"]
     mode = args.mode or cfg["mode"]
     H, W, K = cfg["H"], cfg["W"], cfg["K"]
+    from paper_2005_08165_b200 import dist as tdist
     streaming_cfg = cfg.get("stream", False)
-    per_rank = cfg["frames"] // ws if streaming_cfg else cfg["frames"]
+    if streaming_cfg:          # config 5: a fixed total, sharded by frame over the ranks
+        first, last = tdist.shard(cfg["frames"], rank, ws)
+    else:                      # weak scaling: every rank renders its own batch
+        first, last = rank * cfg["frames"], (rank + 1) * cfg["frames"]
+    per_rank = last - first
     chunk = min(per_rank, 1024) if streaming_cfg else per_rank
-    first = rank * per_rank
 
     est = tfn.Estimator(K, filter=filt, nz_mode=mode, layout=args.layout, kernel=args.kernel,
                         strip_h=args.strip_h, grid=args.grid)
@@ -303,23 +307,22 @@ def main():
     torch.cuda.synchronize()
 
     steps = args.steps
-    n_chunks = (per_rank + chunk - 1) // chunk if streaming_cfg else 1
+    chunk_list = list(tdist.chunks(first, last, chunk))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     launches0 = tfn.tfn_kernel_launches()
     acc = torch.zeros(8, dtype=torch.int64, device=dev)
     clk = ClockSampler(local)
     if streaming_cfg:
         # config 5: per rank, chunks of 1024 frames: render (untimed) -> estimate (timed) -> stats
-        steps = n_chunks
+        steps = len(chunk_list)
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         kernel_ms = 0.0
         if pg:
             pg.barrier()
         torch.cuda.synchronize()
         with clk:
-            for c in range(n_chunks):
-                lo = first + c * chunk
-                n = min(chunk, first + per_rank - lo)
+            for c, (lo, hi) in enumerate(chunk_list):
+                n = hi - lo
                 if c > 0:
                     x, gt = make_frames(cfg, n, lo, args.seed, dev)
                     if out.shape[0] != n:
@@ -358,7 +361,7 @@ def main():
     if pg:
         pg.all_reduce(t_max, op=pg.ReduceOp.MAX)
     total_ms_max = float(t_max.item())
-    all_units = units * ws
+    all_units = cfg["frames"] * H * W if streaming_cfg else units * ws
     value = all_units / (total_ms_max / 1e3) / 1e6           # Mpixel/s whole job
     per_launch_ms = kernel_ms / steps
     px_per_launch = (chunk if not streaming_cfg else chunk) * H * W
@@ -368,14 +371,12 @@ def main():
     # a8 accuracy statistics vs analytic GT (off the timed region), NCCL all-reduce of int64
     if not streaming_cfg and not args.profile:
         tfn.stats(out, gt, layout=args.layout, acc=acc, stream=stream)
-    if pg:
-        pg.all_reduce(acc)
-    st = acc.cpu().numpy().astype(np.int64)
-    m = int(st[1])
+    tdist.allreduce_stats(acc)                 # the only collective (NCCL, int64 SUM)
+    st = acc.cpu().tolist()
     accuracy = None
-    if m > 0:
-        accuracy = {"aae_deg": st[0] / 1e6 / m, "pgp10": st[2] / m, "pgp20": st[3] / m, "pgp30": st[4] / m,
-                    "m": m, "stats_int64": [int(v) for v in st]}
+    if st[1] > 0:
+        accuracy = tdist.summarize(st)
+        accuracy["stats_int64"] = st
 
     # e2e through the public host-buffer API (pinned host in/out, H2D + D2H inside the timed region)
     e2e = None
