@@ -107,10 +107,11 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
         int sh = h->strip_h;
         const long long sx_n = (W + 127) / 128;
         if (sh <= 0) {
-            // 32 rows per strip amortises the 2 halo rows; shrink it when the batch is
-            // too small to give every resident warp a few strips
-            sh = 32;
-            while (sh > 4 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 2 * resident_warps) sh >>= 1;
+            // 24 rows per strip (a multiple of the 3-row unroll; measured best with 12-24 on
+            // config 2); shrink it when the batch is too small to give every resident warp
+            // a few strips
+            sh = 24;
+            while (sh > 6 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 2 * resident_warps) sh /= 2;
         }
         a.strip_h = sh;
         const long long items = sx_n * ((H + sh - 1) / sh) * (long long)batch;

@@ -45,7 +45,8 @@ __global__ void __launch_bounds__(256) tfn_pixel_kernel(KernelArgs p) {
 template <int F, int MODE, bool DISP>
 static cudaError_t launch_t(const KernelArgs& a, int kernel, int grid_strip, cudaStream_t st) {
     if (kernel == TFN_KERNEL_STRIP) {
-        tfn_strip_kernel<F, MODE, DISP><<<grid_strip, TFN_STRIP_THREADS, 0, st>>>(a);
+        if (a.layout == 0) tfn_strip_kernel<F, MODE, DISP, 0><<<grid_strip, TFN_STRIP_THREADS, 0, st>>>(a);
+        else tfn_strip_kernel<F, MODE, DISP, 1><<<grid_strip, TFN_STRIP_THREADS, 0, st>>>(a);
     } else {
         dim3 blk(32, 8, 1);
         dim3 grd((a.W + 31) / 32, (a.H + 7) / 8, (unsigned)a.B);
@@ -65,7 +66,7 @@ static cudaError_t launch_f(const KernelArgs& a, int mode, bool disp, int kernel
 template <int F, int MODE, bool DISP>
 static int occ_t() {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tfn_strip_kernel<F, MODE, DISP>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tfn_strip_kernel<F, MODE, DISP, 0>,
                                                       TFN_STRIP_THREADS, 0) != cudaSuccess) {
         cudaGetLastError();
         return 1;

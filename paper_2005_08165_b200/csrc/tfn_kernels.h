@@ -3,7 +3,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#ifndef TFN_STRIP_THREADS
 #define TFN_STRIP_THREADS 128
+#endif
 #ifndef TFN_STRIP_MINBLOCKS
 #define TFN_STRIP_MINBLOCKS 3
 #endif

@@ -16,7 +16,8 @@
 // Fast path: all 8 candidates finite and Phi != 0 (no skips, no flat rule, no
 // orientation tie, valid pixel).  Anything else ("special": holes, invalid samples,
 // dZ == 0, flat, ties) takes the general per-pixel code behind ONE warp vote per
-// row step.  Known-invalid border pixels are patched to NaN by mask.
+// row step.  Border pixels are never special: their out-of-image taps are NaN, so the
+// fast path already writes the canonical NaN.
 #pragma once
 
 namespace tfn {
@@ -46,7 +47,7 @@ struct StripCtx {
 // predicated off outside the image (never an out-of-bounds address)
 __device__ __forceinline__ void load_raw(Slot& s, const StripCtx& c, int v) {
     s.rok = (v >= 0) && (v < c.H);
-    const float* row = c.pm + (long long)v * c.W;
+    const float* row = c.pm + v * c.W;
     if (s.rok) {
         const float4 m = __ldg(reinterpret_cast<const float4*>(row));
         s.raw[1] = m.x; s.raw[2] = m.y; s.raw[3] = m.z; s.raw[4] = m.w;
@@ -86,7 +87,7 @@ __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d
 
 // One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw receives row
 // v+2), C = slot(v), N = slot(v+1) (N.raw loaded; everything else computed here).
-template <int F, int MODE, bool DISP>
+template <int F, int MODE, bool DISP, int LAYOUT>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx& c,
                                          float* __restrict__ out, long long HW, int layout,
                                          unsigned colmask, float vf) {
@@ -218,13 +219,13 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     }
     // ---- store (16-B aligned: W % 4 == 0, c0 % 4 == 0) ----
     if (c.okm) {
-        float* o = out + (long long)v * c.W;
-        if (layout == 0) {
+        float* o = out + v * c.W;
+        if (LAYOUT == 0) {
             st4(o, nx[0], nx[1], nx[2], nx[3]);
             st4(o + HW, ny[0], ny[1], ny[2], ny[3]);
             st4(o + 2 * HW, nz[0], nz[1], nz[2], nz[3]);
         } else {
-            o += (long long)v * c.W * 2;     // packed: 3 floats per pixel
+            o += v * c.W * 2;     // packed: 3 floats per pixel
             st4(o, nx[0], ny[0], nz[0], nx[1]);
             st4(o + 4, ny[1], nz[1], nx[2], ny[2]);
             st4(o + 8, nz[2], nx[3], ny[3], nz[3]);
@@ -232,7 +233,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     }
 }
 
-template <int F, int MODE, bool DISP>
+template <int F, int MODE, bool DISP, int LAYOUT>
 __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_strip_kernel(KernelArgs p) {
     const int lane = threadIdx.x & 31;
     const int warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -269,7 +270,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
             if (c0 == 0) colmask |= 1u;
             if (c0 + 3 == p.W - 1) colmask |= 8u;
         }
-        float* out = p.out + fb * 3 * HW + (p.layout == 0 ? (long long)c.cm : 3LL * c.cm);
+        float* out = p.out + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm);
 
         Slot S0, S1, S2;
         // prologue: rows y0-1 (S0), y0 (S1) prepared; row y0+1 (S2) loaded
@@ -289,13 +290,13 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
         }
         float vf = __int2float_rn(y0);      // exact row index as float (rows < 2^24)
         for (int v = y0; v < y1; v += 3) {
-            row_step<F, MODE, DISP>(S0, S1, S2, v, c, out, HW, p.layout, colmask, vf);
+            row_step<F, MODE, DISP, LAYOUT>(S0, S1, S2, v, c, out, HW, p.layout, colmask, vf);
             __syncwarp();
             if (v + 1 >= y1) break;
-            row_step<F, MODE, DISP>(S1, S2, S0, v + 1, c, out, HW, p.layout, colmask, vf + 1.0f);
+            row_step<F, MODE, DISP, LAYOUT>(S1, S2, S0, v + 1, c, out, HW, p.layout, colmask, vf + 1.0f);
             __syncwarp();
             if (v + 2 >= y1) break;
-            row_step<F, MODE, DISP>(S2, S0, S1, v + 2, c, out, HW, p.layout, colmask, vf + 2.0f);
+            row_step<F, MODE, DISP, LAYOUT>(S2, S0, S1, v + 2, c, out, HW, p.layout, colmask, vf + 2.0f);
             __syncwarp();
             vf += 3.0f;
         }
