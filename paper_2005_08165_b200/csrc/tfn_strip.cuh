@@ -28,7 +28,7 @@ struct Slot {
     float z[6];        // sanitized (invalid -> NaN)
     double w[6];       // x = 1/z (depth) or d (disparity), fp64
     double head[4];    // kp*D_h(row-1) + k0*D_h(row)   (D_h re-derived from w when needed)
-    float rN[4], rNW[4], rNE[4];   // rho of the N / NW / NE neighbours of this row's pixels
+    float rN[4], rNW[4], rNE[4];   // pair reciprocals of the N / NW / NE neighbours (pairs owned by the row above)
 };
 
 struct StripCtx {
@@ -56,14 +56,12 @@ __device__ __forceinline__ void load_raw(Slot& s, const StripCtx& c, int v) {
     if (s.rok && c.okr) s.raw[5] = __ldg(row + 4);
 }
 
-// Q5 for the fast path.  Depth: z >= FLT_MIN rejects 0, negatives, NaN and
-// subnormals; z = +inf is rejected downstream (its rho is NaN, or, as a centre, all
-// its candidates are 0 so Phi == 0) -> the exact per-pixel path.  Disparity also
-// needs the explicit upper bound (+inf is not caught downstream there).
+// Q5 for the fast path: valid iff finite and >= FLT_MIN (rejects 0, negatives, NaN,
+// +-Inf, subnormals).  An invalid sample becomes NaN, which makes every candidate that
+// uses it NaN and so sends the pixel to the exact path.
 template <bool DISP>
 __device__ __forceinline__ float sanitize_fast(float z, bool ok) {
-    const bool v = DISP ? (ok && z >= 1.17549435e-38f && z <= 3.40282347e+38f) : (ok && z >= 1.17549435e-38f);
-    return v ? z : __int_as_float(0x7fffffff);
+    return (ok && z >= 1.17549435e-38f && z <= 3.40282347e+38f) ? z : __int_as_float(0x7fffffff);
 }
 
 template <bool DISP>
@@ -128,7 +126,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     float rSWp = pair_rcp<DISP>(C.z[1], N.z[0]);
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-        float rho[2][8];
+        float R[2][8];      // pair reciprocals of the 8 neighbours, order E W S N SE NW SW NE
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int i = 2 * q + h;
@@ -137,43 +135,54 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
             const float rS = pair_rcp<DISP>(zc, N.z[i + 1]);
             const float rSE = pair_rcp<DISP>(zc, N.z[i + 2]);
             const float rSW = pair_rcp<DISP>(C.z[i + 2], N.z[i + 1]);
-            rho[h][0] = rho_owner<DISP>(zc, C.z[i + 2], rE);
-            rho[h][1] = rho_other<DISP>(C.z[i], zc, rEp);
-            rho[h][2] = rho_owner<DISP>(zc, N.z[i + 1], rS);
-            rho[h][3] = C.rN[i];
-            rho[h][4] = rho_owner<DISP>(zc, N.z[i + 2], rSE);
-            rho[h][5] = C.rNW[i];
-            rho[h][6] = rho_owner<DISP>(zc, N.z[i], rSWp);
-            rho[h][7] = C.rNE[i];
-            N.rN[i] = rho_other<DISP>(zc, N.z[i + 1], rS);
-            N.rNW[i] = rho_other<DISP>(C.z[i], N.z[i + 1], rSEp);
-            N.rNE[i] = rho_other<DISP>(C.z[i + 2], N.z[i + 1], rSW);
+            R[h][0] = rE;  R[h][1] = rEp;  R[h][2] = rS;  R[h][3] = C.rN[i];
+            R[h][4] = rSE; R[h][5] = C.rNW[i]; R[h][6] = rSWp; R[h][7] = C.rNE[i];
+            // the next row's N / NW / NE pairs are owned by this row
+            N.rN[i] = rS; N.rNW[i] = rSEp; N.rNE[i] = rSW;
             rEp = rE; rSEp = rSE; rSWp = rSW;
         }
         const int i0 = 2 * q, i1 = 2 * q + 1;
         const float2 mu = f2(gu32[i0], gu32[i1]), mv = f2(gv32[i0], gv32[i1]);
         const float2 ms = f2(s32[i0], s32[i1]), mt = f2(t32[i0], t32[i1]);
+        const float2 zc2 = f2(C.z[i0 + 1], C.z[i1 + 1]);
+        // m~ = m * own sample (tfn_device.cuh: tau_owner / tau_other)
+        const float2 xu = __fmul2_rn(mu, zc2), xv = __fmul2_rn(mv, zc2);
+        const float2 xs = __fmul2_rn(ms, zc2), xt = __fmul2_rn(mt, zc2);
         float2 tau[8];
+        float2 sum8;
+        if (DISP) {
 #pragma unroll
-        for (int k = 0; k < 8; k += 2) {
-            const float2 m = (k < 2) ? mu : (k < 4) ? mv : (k < 6) ? ms : mt;
-            tau[k] = __fmul2_rn(m, f2(rho[0][k], rho[1][k]));
+            for (int k = 0; k < 8; k += 2) {
+                const float2 x = (k < 2) ? xu : (k < 4) ? xv : (k < 6) ? xs : xt;
+                tau[k] = __fmul2_rn(x, f2(R[0][k], R[1][k]));
+            }
+            // finish32's explicit-FMA sum
+            const float2 s01 = __ffma2_rn(xu, f2(R[0][1], R[1][1]), tau[0]);
+            const float2 s23 = __ffma2_rn(xv, f2(R[0][3], R[1][3]), tau[2]);
+            const float2 s45 = __ffma2_rn(xs, f2(R[0][5], R[1][5]), tau[4]);
+            const float2 s67 = __ffma2_rn(xt, f2(R[0][7], R[1][7]), tau[6]);
+            sum8 = __fadd2_rn(__fadd2_rn(s01, s23), __fadd2_rn(s45, s67));
+            if (MODE == MEDIAN) {
+#pragma unroll
+                for (int k = 1; k < 8; k += 2) {
+                    const float2 x = (k < 2) ? xu : (k < 4) ? xv : (k < 6) ? xs : xt;
+                    tau[k] = __fmul2_rn(x, f2(R[0][k], R[1][k]));
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float2 x = (k < 2) ? xu : (k < 4) ? xv : (k < 6) ? xs : xt;
+                const float2 m = (k < 2) ? mu : (k < 4) ? mv : (k < 6) ? ms : mt;
+                tau[k] = __ffma2_rn(x, f2(R[0][k], R[1][k]), (k & 1) ? f2(-m.x, -m.y) : m);
+            }
+            sum8 = __fadd2_rn(__fadd2_rn(__fadd2_rn(tau[0], tau[1]), __fadd2_rn(tau[2], tau[3])),
+                              __fadd2_rn(__fadd2_rn(tau[4], tau[5]), __fadd2_rn(tau[6], tau[7])));
         }
-        // the same sum as finish32(): ((fma(m,r1,t0) + fma(m,r3,t2)) + (fma(m,r5,t4) + fma(m,r7,t6)))
-        const float2 s01 = __ffma2_rn(mu, f2(rho[0][1], rho[1][1]), tau[0]);
-        const float2 s23 = __ffma2_rn(mv, f2(rho[0][3], rho[1][3]), tau[2]);
-        const float2 s45 = __ffma2_rn(ms, f2(rho[0][5], rho[1][5]), tau[4]);
-        const float2 s67 = __ffma2_rn(mt, f2(rho[0][7], rho[1][7]), tau[6]);
-        const float2 sum8 = __fadd2_rn(__fadd2_rn(s01, s23), __fadd2_rn(s45, s67));
         float2 phi;
         if (MODE == MEAN) {
             phi = __fmul2_rn(sum8, f2(0.125f, 0.125f));
         } else {
-#pragma unroll
-            for (int k = 1; k < 8; k += 2) {
-                const float2 m = (k < 2) ? mu : (k < 4) ? mv : (k < 6) ? ms : mt;
-                tau[k] = __fmul2_rn(m, f2(rho[0][k], rho[1][k]));
-            }
             float t0[8], t1[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) { t0[k] = tau[k].x; t1[k] = tau[k].y; }
@@ -284,9 +293,9 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
             S1.head[i] = grad_head<F>(Taps<F>::corners ? __dsub_rn(S0.w[i + 2], S0.w[i]) : 0.0,
                                       __dsub_rn(S1.w[i + 2], S1.w[i]));
             const float zc = S1.z[i + 1];
-            S1.rN[i] = rho_other<DISP>(S0.z[i + 1], zc, pair_rcp<DISP>(S0.z[i + 1], zc));
-            S1.rNW[i] = rho_other<DISP>(S0.z[i], zc, pair_rcp<DISP>(S0.z[i], zc));
-            S1.rNE[i] = rho_other<DISP>(S0.z[i + 2], zc, pair_rcp<DISP>(S0.z[i + 2], zc));
+            S1.rN[i] = pair_rcp<DISP>(S0.z[i + 1], zc);
+            S1.rNW[i] = pair_rcp<DISP>(S0.z[i], zc);
+            S1.rNE[i] = pair_rcp<DISP>(S0.z[i + 2], zc);
         }
         float vf = __int2float_rn(y0);      // exact row index as float (rows < 2^24)
         for (int v = y0; v < y1; v += 3) {
