@@ -83,13 +83,14 @@ __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d
     __stcs(reinterpret_cast<float4*>(p), make_float4(a, b, c, d));
 }
 
-// One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw receives row
-// v+2), C = slot(v), N = slot(v+1) (N.raw loaded; everything else computed here).
+// One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw holds row v+2 in
+// flight), C = slot(v) (C.raw receives row v+3), N = slot(v+1) (N.raw loaded; the rest
+// computed here).
 template <int F, int MODE, bool DISP, int LAYOUT>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx& c,
                                          float* __restrict__ out, long long HW, int layout,
                                          unsigned colmask, float vf) {
-    load_raw(P, c, v + 2);                       // prefetch two rows ahead
+    load_raw(C, c, v + 3);                       // prefetch three rows ahead (C.raw is free)
     prepare<DISP>(N, c);
 
     // ---- fp64 gradients (Eq. 15), oracle order (Q10) ----
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
         load_raw(S2, c, y0 + 1);
         prepare<DISP>(S0, c);
         prepare<DISP>(S1, c);
+        load_raw(S0, c, y0 + 2);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             S1.head[i] = grad_head<F>(Taps<F>::corners ? __dsub_rn(S0.w[i + 2], S0.w[i]) : 0.0,
