@@ -94,16 +94,19 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic(cfg_id, filt, mode, layout):
-    """dram bytes/launch from the committed ncu --set full capture, if any."""
+def load_traffic(cfg_id, filt, mode, layout, px_per_launch):
+    """DRAM bytes (read + write, GB) per launch of the same kernel/launch size, from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
         e = d.get(f"config{cfg_id}:{filt}:{mode}:{layout}")
-        return e
+        if e and int(e["launch_px"]) == int(px_per_launch):
+            return float(e["GB_per_launch"])
     except Exception:
-        return None
+        pass
+    return None
 
 
 class ClockSampler:
@@ -407,7 +410,7 @@ def main():
         cpu = cpu_baseline(cfg, filt, mode, args.cpu_seconds, args.seed)
 
     if rank == 0:
-        traffic = load_traffic(args.config, filt, mode, args.layout)
+        traffic = load_traffic(args.config, filt, mode, args.layout, px_per_launch)
         line = {
             "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": ws, "steps": steps,
             "warmup": args.warmup, "ms_per_step": total_ms_max / steps, "higher_is_better": True,
@@ -419,7 +422,8 @@ def main():
                        "l2": "inputs (%.2f GB/GPU) larger than the 126 MB L2; no flush" % (chunk * H * W * 4 / 1e9),
                        "parallelism": f"dp{ws} (frame batches sharded, no collective on the hot path)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_unit": "GB/launch (ncu dram read+write)",
+                         "algorithmic_GB_per_launch": BYTES_PER_PX * px_per_launch / 1e9,
                          "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
                          "kernel": "tfn_strip_kernel", "bytes_per_px": BYTES_PER_PX,
                          "px_per_launch": px_per_launch, "launch_ms": per_launch_ms},
