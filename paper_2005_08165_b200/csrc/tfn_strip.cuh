@@ -207,8 +207,11 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         const float2 sc = f2(r0, r1);
         const float2 ox = __fmul2_rn(px, sc), oy = __fmul2_rn(py, sc), oz = __fmul2_rn(pz, sc);
         nx[i0] = ox.x; nx[i1] = ox.y; ny[i0] = oy.x; ny[i1] = oy.y; nz[i0] = oz.x; nz[i1] = oz.y;
-        const bool sp0 = !(fabsf(sum8.x) < __int_as_float(0x7f800000)) || (phi.x == 0.f);
-        const bool sp1 = !(fabsf(sum8.y) < __int_as_float(0x7f800000)) || (phi.y == 0.f);
+        // special: a non-finite candidate or Phi == 0 at a pixel whose centre is valid (an
+        // invalid centre poisons every candidate through m~ = m * NaN: the fast path
+        // already wrote the canonical NaN)
+        const bool sp0 = (!(fabsf(sum8.x) < __int_as_float(0x7f800000)) || (phi.x == 0.f)) && !isnan(zc2.x);
+        const bool sp1 = (!(fabsf(sum8.y) < __int_as_float(0x7f800000)) || (phi.y == 0.f)) && !isnan(zc2.y);
         special |= (sp0 ? (1u << i0) : 0u) | (sp1 ? (1u << i1) : 0u);
     }
 
