@@ -118,6 +118,13 @@ int tfn_stats(const float* est, const float* gt, int batch, int H, int W, int la
 int tfn_debug_phi8(const float* cand_dev, long long n, int nz_mode, float* out_dev, int* k_dev,
                    void* stream);
 
+/* Speed-of-light reference for the roofline: moves exactly the 3F2N
+ * traffic mix — reads in_dev fp32 [batch,H,W], writes every sample three times into
+ * out_dev fp32 [batch,3,H,W] (planar), 4 B in + 12 B out per pixel, with the strip
+ * kernel's access pattern and no arithmetic.  H*W % 4 == 0 and 16-B aligned buffers
+ * (INVALID_ARGUMENT otherwise).  Asynchronous on stream. */
+int tfn_debug_sol(const float* in_dev, int batch, int H, int W, void* stream, float* out_dev);
+
 /* Release a handle (and its workspace).  NULL is OK. */
 int tfn_destroy(tfn_handle h);
 

@@ -8,7 +8,7 @@ CUDA kernels behind the C ABI include/tfn.h (libtfn.so), with a thin ctypes bind
 
 See DESIGN.md for the method, the boundary and the kernel design.
 """
-from .tfn import (ABI_SYMBOLS, Estimator, TfnError, debug_phi8, lib, stats, tfn_create,  # noqa: F401
+from .tfn import (ABI_SYMBOLS, Estimator, TfnError, debug_phi8, debug_sol, lib, stats, tfn_create,  # noqa: F401
                   tfn_debug_phi8, tfn_destroy, tfn_estimate, tfn_estimate_disparity, tfn_estimate_host,
                   tfn_kernel_launches, tfn_set_layout, tfn_set_option, tfn_stats, tfn_status_string,
                   tfn_version, STAT_KEYS, LIB_PATH)

@@ -289,6 +289,18 @@ TFN_API int tfn_debug_phi8(const float* cand_dev, long long n, int nz_mode, floa
     return TFN_OK;
 }
 
+TFN_API int tfn_debug_sol(const float* in_dev, int batch, int H, int W, void* stream, float* out_dev) {
+    if (batch < 0 || H <= 0 || W <= 0) return TFN_ERR_INVALID_ARGUMENT;
+    if (batch == 0) return TFN_OK;
+    if (!in_dev || !out_dev || ((long long)H * W) % 4 || ((uintptr_t)in_dev & 15) || ((uintptr_t)out_dev & 15))
+        return TFN_ERR_INVALID_ARGUMENT;
+    int dev = 0, sms = 0;
+    if (check_device(&dev, &sms) != TFN_OK) return TFN_ERR_CUDA;
+    if (tfn::launch_sol(in_dev, out_dev, batch, H, W, sms, (cudaStream_t)stream) != cudaSuccess) return TFN_ERR_CUDA;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return TFN_OK;
+}
+
 TFN_API int tfn_destroy(tfn_handle h) {
     if (!h) return TFN_OK;
     {

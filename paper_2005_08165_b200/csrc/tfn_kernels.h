@@ -35,6 +35,9 @@ int strip_occupancy(int filter, int mode, bool disp);
 cudaError_t launch_stats(const float* est, const float* gt, long long B, int H, int W,
                          int layout, long long* stats_dev, cudaStream_t st);
 
+// SOL reference for the traffic mix (4 B in, 12 B out per pixel)
+cudaError_t launch_sol(const float* in, float* out, long long B, int H, int W, int sms, cudaStream_t st);
+
 // P8 probe: Phi of n groups of 8 candidates (non-finite = skipped)
 cudaError_t launch_phi8(const float* cand, long long n, int mode, float* out, int* k_out,
                         cudaStream_t st);

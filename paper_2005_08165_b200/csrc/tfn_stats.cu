@@ -77,6 +77,33 @@ cudaError_t launch_stats(const float* est, const float* gt, long long B, int H, 
     return cudaGetLastError();
 }
 
+// Speed-of-light reference for the 3F2N traffic mix: 4 B read + 12 B
+// written per pixel with the strip kernel's access pattern (one LDG.128 per lane-row,
+// three streaming STG.128 into the planar normal map), no arithmetic.
+__global__ void __launch_bounds__(256) tfn_sol_kernel(const float4* __restrict__ in, float4* __restrict__ out,
+                                                     long long quads_per_frame, long long frames) {
+    const long long n = quads_per_frame * frames;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long f = i / quads_per_frame, q = i - f * quads_per_frame;
+        const float4 z = __ldg(in + i);
+        float4* o = out + f * 3 * quads_per_frame + q;
+        __stcs(o, z);
+        __stcs(o + quads_per_frame, z);
+        __stcs(o + 2 * quads_per_frame, z);
+    }
+}
+
+cudaError_t launch_sol(const float* in, float* out, long long B, int H, int W, int sms, cudaStream_t st) {
+    const long long qpf = (long long)H * W / 4;
+    long long blocks = (qpf * B + 255) / 256;
+    if (blocks > (long long)sms * 8) blocks = (long long)sms * 8;
+    if (blocks < 1) blocks = 1;
+    tfn_sol_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(in),
+                                                      reinterpret_cast<float4*>(out), qpf, B);
+    return cudaGetLastError();
+}
+
 template <int MODE>
 __global__ void tfn_phi8_kernel(const float* __restrict__ cand, long long n, float* out, int* kout) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;

@@ -31,7 +31,7 @@ OPT_KERNEL, OPT_STRIP_H, OPT_GRID = 0, 1, 2
 ABI_SYMBOLS = (
     "tfn_create", "tfn_set_layout", "tfn_set_option", "tfn_estimate", "tfn_estimate_disparity",
     "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8", "tfn_destroy", "tfn_status_string",
-    "tfn_kernel_launches", "tfn_version",
+    "tfn_kernel_launches", "tfn_version", "tfn_debug_sol",
 )
 
 
@@ -66,6 +66,7 @@ def lib() -> ctypes.CDLL:
         L.tfn_estimate_host.argtypes = [vp, vp, i, d, i, i, i, vp, vp]
         L.tfn_stats.argtypes = [vp, vp, i, i, i, i, vp, vp]
         L.tfn_debug_phi8.argtypes = [vp, ll, i, vp, vp, vp]
+        L.tfn_debug_sol.argtypes = [vp, i, i, i, vp, vp]
         L.tfn_destroy.argtypes = [vp]
         L.tfn_status_string.argtypes = [i]
         L.tfn_status_string.restype = ctypes.c_char_p
@@ -75,7 +76,7 @@ def lib() -> ctypes.CDLL:
             if f.restype is ctypes.c_int or name in ("tfn_create", "tfn_set_layout", "tfn_set_option",
                                                      "tfn_estimate", "tfn_estimate_disparity",
                                                      "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8",
-                                                     "tfn_destroy", "tfn_version"):
+                                                     "tfn_destroy", "tfn_version", "tfn_debug_sol"):
                 f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -132,6 +133,16 @@ def tfn_stats(est_ptr: int, gt_ptr: int, batch: int, H: int, W: int, layout: int
 
 def tfn_debug_phi8(cand_ptr: int, n: int, nz_mode: int, out_ptr: int, k_ptr: int, stream: int) -> int:
     return lib().tfn_debug_phi8(cand_ptr, n, nz_mode, out_ptr, k_ptr, stream)
+
+
+def tfn_debug_sol(in_ptr: int, batch: int, H: int, W: int, stream: int, out_ptr: int) -> int:
+    return lib().tfn_debug_sol(in_ptr, batch, H, W, stream, out_ptr)
+
+
+def debug_sol(x: torch.Tensor, out: torch.Tensor, stream: Optional[torch.cuda.Stream] = None) -> None:
+    """SOL traffic-mix copy (4 B in, 12 B out per pixel), for the roofline context."""
+    B, H, W = _bhw(x)
+    _check(tfn_debug_sol(x.data_ptr(), B, H, W, _stream_ptr(stream), out.data_ptr()), "tfn_debug_sol")
 
 
 def tfn_destroy(h: int) -> int:
