@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel"])
     ap.add_argument("--strip-h", type=int, default=0)
     ap.add_argument("--grid", type=int, default=0)
+    ap.add_argument("--static", action="store_true", help="static strip scheduling")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -296,7 +297,7 @@ def main():
     chunk = min(per_rank, 1024) if streaming_cfg else per_rank
 
     est = tfn.Estimator(K, filter=filt, nz_mode=mode, layout=args.layout, kernel=args.kernel,
-                        strip_h=args.strip_h, grid=args.grid)
+                        strip_h=args.strip_h, grid=args.grid, dynamic=not args.static)
     stream = torch.cuda.current_stream(dev)
 
     def launch(x, out):

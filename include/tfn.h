@@ -62,7 +62,8 @@ typedef enum { TFN_LAYOUT_PLANAR = 0, TFN_LAYOUT_PACKED = 1 } tfn_layout;
 typedef enum {
     TFN_OPT_KERNEL = 0,     /* 0 auto, 1 per-pixel kernel, 2 strip kernel (needs W%4==0, 16-B alignment) */
     TFN_OPT_STRIP_H = 1,    /* rows per warp strip, 0 = auto (>= 4)                                        */
-    TFN_OPT_GRID = 2        /* CTAs of the strip kernel, 0 = auto (resident CTAs x SMs)                    */
+    TFN_OPT_GRID = 2,       /* CTAs of the strip kernel, 0 = auto (resident CTAs x SMs)                    */
+    TFN_OPT_DYNAMIC = 3     /* 1 (default): strips claimed from a per-call work counter; 0: static stride  */
 } tfn_option;
 
 /* Pinhole intrinsics in pixels (Eq. 13): u = column, v = row, 0-based, pixel

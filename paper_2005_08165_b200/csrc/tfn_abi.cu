@@ -37,12 +37,16 @@ struct tfn_ctx {
     int kernel = tfn::TFN_KERNEL_AUTO;
     int strip_h = 0;
     int grid = 0;
+    int dynamic = 1;
     int device = 0;
     int sms = 148;
     int strip_ctas_per_sm[2] = {0, 0};   // depth, disparity
     std::mutex ws_mu;
     Workspace ws;
+    int* work = nullptr;                 // ring of per-call work counters (dynamic scheduling)
+    std::atomic<unsigned> call_seq{0};
 };
+#define TFN_WORK_RING 4096
 
 namespace {
 
@@ -114,6 +118,12 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
             while (sh > 6 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 2 * resident_warps) sh /= 2;
         }
         a.strip_h = sh;
+        a.work = nullptr;
+        if (h->work && h->dynamic) {
+            int* ctr = h->work + (h->call_seq.fetch_add(1) % TFN_WORK_RING);
+            if (cudaMemsetAsync(ctr, 0, sizeof(int), st) != cudaSuccess) return TFN_ERR_CUDA;
+            a.work = ctr;
+        }
         const long long items = sx_n * ((H + sh - 1) / sh) * (long long)batch;
         long long ctas = h->grid > 0 ? h->grid : (long long)h->sms * h->strip_ctas_per_sm[disp];
         const long long need = (items + (TFN_STRIP_THREADS / 32) - 1) / (TFN_STRIP_THREADS / 32);
@@ -152,6 +162,10 @@ TFN_API int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_han
         h->strip_ctas_per_sm[d] = tfn::strip_occupancy(filter, nz_mode, d != 0);
         if (h->strip_ctas_per_sm[d] <= 0) h->strip_ctas_per_sm[d] = 1;
     }
+    if (cudaMalloc(&h->work, TFN_WORK_RING * sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        h->work = nullptr;                // static scheduling still works
+    }
     *out = h;
     return TFN_OK;
 }
@@ -176,6 +190,9 @@ TFN_API int tfn_set_option(tfn_handle h, int option, long long value) {
     case TFN_OPT_GRID:
         if (value < 0 || value > 1 << 24) return TFN_ERR_INVALID_ARGUMENT;
         h->grid = (int)value;
+        return TFN_OK;
+    case TFN_OPT_DYNAMIC:
+        h->dynamic = value ? 1 : 0;
         return TFN_OK;
     default:
         return TFN_ERR_INVALID_ARGUMENT;
@@ -312,6 +329,7 @@ TFN_API int tfn_destroy(tfn_handle h) {
         }
         if (h->ws.start) cudaEventDestroy(h->ws.start);
     }
+    if (h->work) cudaFree(h->work);
     delete h;
     return TFN_OK;
 }

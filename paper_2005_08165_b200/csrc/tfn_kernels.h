@@ -23,6 +23,7 @@ struct KernelArgs {
     float u0, v0;        // a = u - u0, b = v - v0 (Eq. 13), principal point rounded to fp32
     int layout;
     int strip_h;         // rows per warp strip (strip kernel)
+    int* work;           // zeroed work counter for dynamic strip scheduling (nullptr: static)
 };
 
 cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, int kernel,

@@ -261,7 +261,9 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
     c.fx = p.fx; c.fy = p.fy;
     c.u0 = p.u0; c.v0 = p.v0;
 
-    for (int it = warp0; it < items; it += nwarps) {
+    // first item static, the rest claimed from a work counter (load balance: strips with
+    // holes or sky cost more or less than others); static striding without a counter
+    for (int it = warp0; it < items;) {
         const int sx = it % sx_n;
         const int t2 = it / sx_n;
         const int sy = t2 % sy_n;
@@ -313,6 +315,13 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
             row_step<F, MODE, DISP, LAYOUT>(S2, S0, S1, v + 2, c, out, HW, p.layout, colmask, vf + 2.0f);
             __syncwarp();
             vf += 3.0f;
+        }
+        if (p.work) {
+            int nxt = 0;
+            if (lane == 0) nxt = atomicAdd(p.work, 1);
+            it = nwarps + __shfl_sync(0xffffffffu, nxt, 0);
+        } else {
+            it += nwarps;
         }
     }
 }

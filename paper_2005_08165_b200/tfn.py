@@ -25,7 +25,7 @@ FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3}
 MODES = {"mean": 0, "median": 1}
 LAYOUTS = {"planar": 0, "packed": 1}
 KERNELS = {"auto": 0, "pixel": 1, "strip": 2}
-OPT_KERNEL, OPT_STRIP_H, OPT_GRID = 0, 1, 2
+OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_DYNAMIC = 0, 1, 2, 3
 
 # every symbol include/tfn.h declares (tests/test_abi.py checks the export table)
 ABI_SYMBOLS = (
@@ -182,7 +182,7 @@ class Estimator:
     """One tfn handle: intrinsics K=(fx,fy,u0,v0), gradient kernel, Phi, layout."""
 
     def __init__(self, K, filter: str = "sobel", nz_mode: str = "median", layout: str = "planar",
-                 kernel: str = "auto", strip_h: int = 0, grid: int = 0):
+                 kernel: str = "auto", strip_h: int = 0, grid: int = 0, dynamic: bool = True):
         self.K = K.as_tuple() if hasattr(K, "as_tuple") else tuple(float(x) for x in K)
         self.filter, self.nz_mode, self.layout = filter, nz_mode, layout
         self.h = tfn_create(self.K, FILTERS[filter], MODES[nz_mode])
@@ -190,6 +190,7 @@ class Estimator:
         tfn_set_option(self.h, OPT_KERNEL, KERNELS[kernel])
         tfn_set_option(self.h, OPT_STRIP_H, strip_h)
         tfn_set_option(self.h, OPT_GRID, grid)
+        tfn_set_option(self.h, OPT_DYNAMIC, int(dynamic))
 
     def _out(self, B, H, W, like: torch.Tensor, out):
         shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
