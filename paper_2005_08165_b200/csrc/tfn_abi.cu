@@ -111,10 +111,10 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
         int sh = h->strip_h;
         const long long sx_n = (W + 127) / 128;
         if (sh <= 0) {
-            // 24 rows per strip (a multiple of the 3-row unroll; measured best with 12-24 on
-            // config 2); shrink it when the batch is too small to give every resident warp
-            // a few strips
-            sh = 24;
+            // 48 rows per strip (a multiple of the 3-row unroll; measured best on config 2 with
+            // dynamic scheduling: 12 -> 192.7, 24 -> 201.1, 48 -> 203.3 Gpx/s); halved while
+            // the batch is too small to give every resident warp two strips
+            sh = 48;
             while (sh > 6 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 2 * resident_warps) sh /= 2;
         }
         a.strip_h = sh;
