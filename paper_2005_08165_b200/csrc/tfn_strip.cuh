@@ -61,7 +61,8 @@ __device__ __forceinline__ void load_raw(Slot& s, const StripCtx& c, int v) {
 // uses it NaN and so sends the pixel to the exact path.
 template <bool DISP>
 __device__ __forceinline__ float sanitize_fast(float z, bool ok) {
-    return (ok && z >= 1.17549435e-38f && z <= 3.40282347e+38f) ? z : __int_as_float(0x7fffffff);
+    const bool good = valid_bits(z) & ok;      // no short circuit: FSEL, not a branch
+    return good ? z : __int_as_float(0x7fffffff);
 }
 
 template <bool DISP>
@@ -187,10 +188,10 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
             float t0[8], t1[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) { t0[k] = tau[k].x; t1[k] = tau[k].y; }
-            float L0, U0, L1, U1;
-            mid_pair8(t0, L0, U0);
-            mid_pair8(t1, L1, U1);
-            phi = __ffma2_rn(f2(0.5f, 0.5f), f2(L0, L1), __fmul2_rn(f2(0.5f, 0.5f), f2(U0, U1)));
+            float a0, b0, a1, b1;
+            mid_pair8(t0, a0, b0);
+            mid_pair8(t1, a1, b1);
+            phi = __fmul2_rn(__fadd2_rn(f2(a0, a1), f2(b0, b1)), f2(0.5f, 0.5f));
             // FMNMX drops NaN candidates: make Phi NaN when any candidate is non-finite, so
             // pixels with out-of-image taps (the border, never "special") come out NaN
             phi = __ffma2_rn(f2(0.f, 0.f), sum8, phi);
@@ -247,7 +248,11 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
 }
 
 template <int F, int MODE, bool DISP, int LAYOUT>
+#ifdef TFN_STRIP_MAXNREG
+__global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(KernelArgs p) {
+#else
 __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_strip_kernel(KernelArgs p) {
+#endif
     const int lane = threadIdx.x & 31;
     const int warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -307,13 +312,10 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
         float vf = __int2float_rn(y0);      // exact row index as float (rows < 2^24)
         for (int v = y0; v < y1; v += 3) {
             row_step<F, MODE, DISP, LAYOUT>(S0, S1, S2, v, c, out, HW, p.layout, colmask, vf);
-            __syncwarp();
             if (v + 1 >= y1) break;
             row_step<F, MODE, DISP, LAYOUT>(S1, S2, S0, v + 1, c, out, HW, p.layout, colmask, vf + 1.0f);
-            __syncwarp();
             if (v + 2 >= y1) break;
             row_step<F, MODE, DISP, LAYOUT>(S2, S0, S1, v + 2, c, out, HW, p.layout, colmask, vf + 2.0f);
-            __syncwarp();
             vf += 3.0f;
         }
         if (p.work) {
