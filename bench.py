@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--mode", default=None)
     ap.add_argument("--layout", default="planar", choices=["planar", "packed"])
     ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel", "general"])
     ap.add_argument("--strip-h", type=int, default=0)
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--static", action="store_true", help="static strip scheduling")

@@ -40,13 +40,29 @@ struct tfn_ctx {
     int dynamic = 1;
     int device = 0;
     int sms = 148;
-    int strip_ctas_per_sm[2] = {0, 0};   // depth, disparity
+    int strip_ctas_per_sm[2][2] = {{0, 0}, {0, 0}};   // [fast, general][depth, disparity]
     std::mutex ws_mu;
     Workspace ws;
-    int* work = nullptr;                 // ring of per-call work counters (dynamic scheduling)
+    int* work = nullptr;                 // ring of per-call {work, fired} counter pairs
     std::atomic<unsigned> call_seq{0};
+    // AUTO kernel selection: the fast strip variant counts its special row steps; the count
+    // comes back through a pinned word a few calls later and picks fast vs general
+    std::mutex auto_mu;
+    int* fb_host = nullptr;              // pinned: fired row steps of the last probed launch
+    cudaEvent_t fb_ev = nullptr;
+    bool fb_pending = false;
+    double fb_steps = 0;                 // row steps of that launch
+    int auto_general = 0;                // current AUTO choice: 0 fast, 1 general
+    unsigned auto_calls = 0;
 };
 #define TFN_WORK_RING 4096
+// AUTO: general variant when more than this fraction of the fast variant's row steps needed
+// the special path (measured break-even ~0.24: config 2 has 0.011 and runs 210 vs 160 Gpx/s
+// fast vs general; config 4 (holes + 1 % salt) has 0.98 and runs 92.5 vs 157)
+#define TFN_AUTO_GENERAL_ABOVE 0.20
+#define TFN_AUTO_FAST_BELOW 0.10
+#define TFN_AUTO_PROBE_FAST 8            // fast mode: read the counter back every 8th call
+#define TFN_AUTO_PROBE_GENERAL 32        // general mode: re-probe with the fast variant every 32nd call
 
 namespace {
 
@@ -102,12 +118,33 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
     const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & 15) == 0) && (((uintptr_t)out & 15) == 0) &&
                           max_items < (1LL << 31);
     int kernel = h->kernel;
-    if (kernel == tfn::TFN_KERNEL_AUTO) kernel = strip_ok ? tfn::TFN_KERNEL_STRIP : tfn::TFN_KERNEL_PIXEL;
-    if (kernel == tfn::TFN_KERNEL_STRIP && !strip_ok) return TFN_ERR_INVALID_ARGUMENT;
+    bool probe = false;
+    if (kernel == tfn::TFN_KERNEL_AUTO) {
+        if (!strip_ok) {
+            kernel = tfn::TFN_KERNEL_PIXEL;
+        } else {
+            std::lock_guard<std::mutex> lk(h->auto_mu);
+            if (h->fb_pending && cudaEventQuery(h->fb_ev) == cudaSuccess) {
+                const double rate = h->fb_steps > 0 ? *h->fb_host / h->fb_steps : 0.0;
+                if (rate > TFN_AUTO_GENERAL_ABOVE) h->auto_general = 1;
+                else if (rate < TFN_AUTO_FAST_BELOW) h->auto_general = 0;
+                h->fb_pending = false;
+            }
+            cudaGetLastError();           // a not-ready query is not an error
+            const unsigned n = h->auto_calls++;
+            const bool use_general = h->auto_general && (n % TFN_AUTO_PROBE_GENERAL) != 0;
+            kernel = use_general ? tfn::TFN_KERNEL_STRIP_GENERAL : tfn::TFN_KERNEL_STRIP;
+            probe = !use_general && h->fb_host && !h->fb_pending &&
+                    (h->auto_general || (n % TFN_AUTO_PROBE_FAST) == 0);
+        }
+    }
+    const bool strip = (kernel == tfn::TFN_KERNEL_STRIP || kernel == tfn::TFN_KERNEL_STRIP_GENERAL);
+    if (strip && !strip_ok) return TFN_ERR_INVALID_ARGUMENT;
+    const int gen = (kernel == tfn::TFN_KERNEL_STRIP_GENERAL) ? 1 : 0;
     int grid = 0;
-    if (kernel == tfn::TFN_KERNEL_STRIP) {
+    if (strip) {
         const long long resident_warps =
-            (long long)h->sms * h->strip_ctas_per_sm[disp] * (TFN_STRIP_THREADS / 32);
+            (long long)h->sms * h->strip_ctas_per_sm[gen][disp] * (TFN_STRIP_THREADS / 32);
         int sh = h->strip_h;
         const long long sx_n = (W + 127) / 128;
         if (sh <= 0) {
@@ -119,13 +156,15 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
         }
         a.strip_h = sh;
         a.work = nullptr;
-        if (h->work && h->dynamic) {
-            int* ctr = h->work + (h->call_seq.fetch_add(1) % TFN_WORK_RING);
-            if (cudaMemsetAsync(ctr, 0, sizeof(int), st) != cudaSuccess) return TFN_ERR_CUDA;
-            a.work = ctr;
+        a.fired = nullptr;
+        if (h->work && (h->dynamic || probe)) {
+            int* ctr = h->work + 2 * (h->call_seq.fetch_add(1) % TFN_WORK_RING);
+            if (cudaMemsetAsync(ctr, 0, 2 * sizeof(int), st) != cudaSuccess) return TFN_ERR_CUDA;
+            a.work = h->dynamic ? ctr : nullptr;
+            a.fired = probe ? ctr + 1 : nullptr;
         }
         const long long items = sx_n * ((H + sh - 1) / sh) * (long long)batch;
-        long long ctas = h->grid > 0 ? h->grid : (long long)h->sms * h->strip_ctas_per_sm[disp];
+        long long ctas = h->grid > 0 ? h->grid : (long long)h->sms * h->strip_ctas_per_sm[gen][disp];
         const long long need = (items + (TFN_STRIP_THREADS / 32) - 1) / (TFN_STRIP_THREADS / 32);
         if (ctas > need) ctas = need;
         if (ctas < 1) ctas = 1;
@@ -135,6 +174,16 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
     }
     cudaError_t e = tfn::launch_3f2n(a, h->filter, h->mode, disp, kernel, grid, st);
     if (e != cudaSuccess) return TFN_ERR_CUDA;
+    if (a.fired) {
+        std::lock_guard<std::mutex> lk(h->auto_mu);
+        if (!h->fb_pending &&
+            cudaMemcpyAsync(h->fb_host, a.fired, sizeof(int), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
+            cudaEventRecord(h->fb_ev, st) == cudaSuccess) {
+            h->fb_steps = (double)((W + 127) / 128) * H * (double)batch;
+            h->fb_pending = true;
+        }
+        cudaGetLastError();
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return TFN_OK;
 }
@@ -158,13 +207,21 @@ TFN_API int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_han
     h->mode = nz_mode;
     h->device = dev;
     h->sms = sms;
-    for (int d = 0; d < 2; ++d) {
-        h->strip_ctas_per_sm[d] = tfn::strip_occupancy(filter, nz_mode, d != 0);
-        if (h->strip_ctas_per_sm[d] <= 0) h->strip_ctas_per_sm[d] = 1;
-    }
-    if (cudaMalloc(&h->work, TFN_WORK_RING * sizeof(int)) != cudaSuccess) {
+    for (int g = 0; g < 2; ++g)
+        for (int d = 0; d < 2; ++d) {
+            int& n = h->strip_ctas_per_sm[g][d];
+            n = tfn::strip_occupancy(filter, nz_mode, d != 0, g);
+            if (n <= 0) n = 1;
+        }
+    if (cudaMalloc(&h->work, 2 * TFN_WORK_RING * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
-        h->work = nullptr;                // static scheduling still works
+        h->work = nullptr;                // static scheduling (and the fast AUTO choice) still work
+    }
+    if (cudaMallocHost(&h->fb_host, sizeof(int)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->fb_ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        if (h->fb_host) cudaFreeHost(h->fb_host);
+        h->fb_host = nullptr;             // AUTO then always picks the fast variant
     }
     *out = h;
     return TFN_OK;
@@ -180,7 +237,7 @@ TFN_API int tfn_set_option(tfn_handle h, int option, long long value) {
     if (!h) return TFN_ERR_INVALID_ARGUMENT;
     switch (option) {
     case TFN_OPT_KERNEL:
-        if (value < 0 || value > 2) return TFN_ERR_INVALID_ARGUMENT;
+        if (value < 0 || value > 3) return TFN_ERR_INVALID_ARGUMENT;
         h->kernel = (int)value;
         return TFN_OK;
     case TFN_OPT_STRIP_H:
@@ -330,6 +387,8 @@ TFN_API int tfn_destroy(tfn_handle h) {
         if (h->ws.start) cudaEventDestroy(h->ws.start);
     }
     if (h->work) cudaFree(h->work);
+    if (h->fb_ev) cudaEventDestroy(h->fb_ev);
+    if (h->fb_host) cudaFreeHost(h->fb_host);
     delete h;
     return TFN_OK;
 }
@@ -345,5 +404,12 @@ TFN_API const char* tfn_status_string(int status) {
 }
 
 TFN_API unsigned long long tfn_kernel_launches(void) { return g_launches.load(); }
+
+TFN_API int tfn_auto_variant(tfn_handle h, int* variant) {
+    if (!h || !variant) return TFN_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(h->auto_mu);
+    *variant = h->auto_general ? tfn::TFN_KERNEL_STRIP_GENERAL : tfn::TFN_KERNEL_STRIP;
+    return TFN_OK;
+}
 
 TFN_API int tfn_version(void) { return 100; }

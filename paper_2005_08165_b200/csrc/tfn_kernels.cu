@@ -45,8 +45,11 @@ __global__ void __launch_bounds__(256) tfn_pixel_kernel(KernelArgs p) {
 template <int F, int MODE, bool DISP>
 static cudaError_t launch_t(const KernelArgs& a, int kernel, int grid_strip, cudaStream_t st) {
     if (kernel == TFN_KERNEL_STRIP) {
-        if (a.layout == 0) tfn_strip_kernel<F, MODE, DISP, 0><<<grid_strip, TFN_STRIP_THREADS, 0, st>>>(a);
-        else tfn_strip_kernel<F, MODE, DISP, 1><<<grid_strip, TFN_STRIP_THREADS, 0, st>>>(a);
+        if (a.layout == 0) tfn_strip_kernel<F, MODE, DISP, 0, 0><<<grid_strip, TFN_STRIP_THREADS, 0, st>>>(a);
+        else tfn_strip_kernel<F, MODE, DISP, 1, 0><<<grid_strip, TFN_STRIP_THREADS, 0, st>>>(a);
+    } else if (kernel == TFN_KERNEL_STRIP_GENERAL) {
+        if (a.layout == 0) tfn_strip_kernel<F, MODE, DISP, 0, 1><<<grid_strip, TFN_STRIP_THREADS, 0, st>>>(a);
+        else tfn_strip_kernel<F, MODE, DISP, 1, 1><<<grid_strip, TFN_STRIP_THREADS, 0, st>>>(a);
     } else {
         dim3 blk(32, 8, 1);
         dim3 grd((a.W + 31) / 32, (a.H + 7) / 8, (unsigned)a.B);
@@ -64,26 +67,30 @@ static cudaError_t launch_f(const KernelArgs& a, int mode, bool disp, int kernel
 }
 
 template <int F, int MODE, bool DISP>
-static int occ_t() {
+static int occ_t(int gen) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tfn_strip_kernel<F, MODE, DISP, 0>,
-                                                      TFN_STRIP_THREADS, 0) != cudaSuccess) {
+    const cudaError_t e =
+        gen ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tfn_strip_kernel<F, MODE, DISP, 0, 1>,
+                                                            TFN_STRIP_THREADS, 0)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, tfn_strip_kernel<F, MODE, DISP, 0, 0>,
+                                                            TFN_STRIP_THREADS, 0);
+    if (e != cudaSuccess) {
         cudaGetLastError();
         return 1;
     }
     return n;
 }
 template <int F>
-static int occ_f(int mode, bool disp) {
-    if (mode == MEAN) return disp ? occ_t<F, MEAN, true>() : occ_t<F, MEAN, false>();
-    return disp ? occ_t<F, MEDIAN, true>() : occ_t<F, MEDIAN, false>();
+static int occ_f(int mode, bool disp, int gen) {
+    if (mode == MEAN) return disp ? occ_t<F, MEAN, true>(gen) : occ_t<F, MEAN, false>(gen);
+    return disp ? occ_t<F, MEDIAN, true>(gen) : occ_t<F, MEDIAN, false>(gen);
 }
-int strip_occupancy(int filter, int mode, bool disp) {
+int strip_occupancy(int filter, int mode, bool disp, int gen) {
     switch (filter) {
-    case FD: return occ_f<FD>(mode, disp);
-    case SOBEL: return occ_f<SOBEL>(mode, disp);
-    case SCHARR: return occ_f<SCHARR>(mode, disp);
-    default: return occ_f<PREWITT>(mode, disp);
+    case FD: return occ_f<FD>(mode, disp, gen);
+    case SOBEL: return occ_f<SOBEL>(mode, disp, gen);
+    case SCHARR: return occ_f<SCHARR>(mode, disp, gen);
+    default: return occ_f<PREWITT>(mode, disp, gen);
     }
 }
 

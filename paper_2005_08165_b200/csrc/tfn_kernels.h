@@ -12,7 +12,7 @@
 
 namespace tfn {
 
-enum KernelId { TFN_KERNEL_AUTO = 0, TFN_KERNEL_PIXEL = 1, TFN_KERNEL_STRIP = 2 };
+enum KernelId { TFN_KERNEL_AUTO = 0, TFN_KERNEL_PIXEL = 1, TFN_KERNEL_STRIP = 2, TFN_KERNEL_STRIP_GENERAL = 3 };
 
 struct KernelArgs {
     const float* in;     // [B,H,W] depth or disparity
@@ -24,13 +24,14 @@ struct KernelArgs {
     int layout;
     int strip_h;         // rows per warp strip (strip kernel)
     int* work;           // zeroed work counter for dynamic strip scheduling (nullptr: static)
+    int* fired;          // fast strip variant: += its special row steps (nullptr: not counted)
 };
 
 cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, int kernel,
                         int grid_strip, cudaStream_t st);
 
 // resident CTAs per SM of the strip kernel variant (occupancy query)
-int strip_occupancy(int filter, int mode, bool disp);
+int strip_occupancy(int filter, int mode, bool disp, int variant);   // 0 fast, 1 general
 
 // a8: angular-error statistics vs ground truth (off the timed path)
 cudaError_t launch_stats(const float* est, const float* gt, long long B, int H, int W,

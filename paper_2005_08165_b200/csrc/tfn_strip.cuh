@@ -40,6 +40,7 @@ struct StripCtx {
     bool okm, okl, okr;   // lane's columns / left halo / right halo inside the image
     float fx, fy;
     float a[4];        // u - u0 of the 4 columns
+    int* fired;        // AUTO probe: += 1 per row step that needed the special path
     float v0;
 };
 
@@ -65,7 +66,7 @@ __device__ __forceinline__ float sanitize_fast(float z, bool ok) {
     return good ? z : __int_as_float(0x7fffffff);
 }
 
-template <bool DISP>
+template <bool DISP, bool GEN>
 __device__ __forceinline__ void prepare(Slot& s, const StripCtx& c) {
     s.z[0] = sanitize_fast<DISP>(s.raw[0], s.rok && c.okl);
 #pragma unroll
@@ -74,7 +75,13 @@ __device__ __forceinline__ void prepare(Slot& s, const StripCtx& c) {
     // exact for every valid sample; invalid ones give finite garbage here, but their
     // NaN z makes the pixel "special", which recomputes it exactly
 #pragma unroll
-    for (int j = 0; j < 6; ++j) s.w[j] = DISP ? widen_pos(s.z[j]) : rcp_rn(widen_pos(s.z[j]));
+    for (int j = 0; j < 6; ++j) {
+        double x = widen_pos(s.z[j]);
+        // general variant: an invalid sample's x is NaN (a NaN high word), so every gradient
+        // that uses it is NaN and the pixel comes out invalid (Q4) without a special path
+        if (GEN) x = __hiloint2double(isnan(s.z[j]) ? 0x7ff80000 : __double2hiint(x), __double2loint(x));
+        s.w[j] = DISP ? x : rcp_rn(x);
+    }
 }
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -87,12 +94,12 @@ __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d
 // One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw holds row v+2 in
 // flight), C = slot(v) (C.raw receives row v+3), N = slot(v+1) (N.raw loaded; the rest
 // computed here).
-template <int F, int MODE, bool DISP, int LAYOUT>
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx& c,
                                          float* __restrict__ out, long long HW, int layout,
                                          unsigned colmask, float vf) {
     load_raw(C, c, v + 3);                       // prefetch three rows ahead (C.raw is free)
-    prepare<DISP>(N, c);
+    prepare<DISP, GEN>(N, c);
 
     // ---- fp64 gradients (Eq. 15), oracle order (Q10) ----
     double gu[4], gv[4];
@@ -164,7 +171,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
             const float2 s45 = __ffma2_rn(xs, f2(R[0][5], R[1][5]), tau[4]);
             const float2 s67 = __ffma2_rn(xt, f2(R[0][7], R[1][7]), tau[6]);
             sum8 = __fadd2_rn(__fadd2_rn(s01, s23), __fadd2_rn(s45, s67));
-            if (MODE == MEDIAN) {
+            if (MODE == MEDIAN || GEN) {     // the general variant also needs every candidate
 #pragma unroll
                 for (int k = 1; k < 8; k += 2) {
                     const float2 x = (k < 2) ? xu : (k < 4) ? xv : (k < 6) ? xs : xt;
@@ -180,6 +187,23 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
             }
             sum8 = __fadd2_rn(__fadd2_rn(__fadd2_rn(tau[0], tau[1]), __fadd2_rn(tau[2], tau[3])),
                               __fadd2_rn(__fadd2_rn(tau[4], tau[5]), __fadd2_rn(tau[6], tau[7])));
+        }
+        if (GEN) {
+            // general variant: skipped candidates, flat, ties and invalid pixels handled in
+            // registers by the same code as the per-pixel kernel (bit-identical results)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int i = 2 * q + h;
+                float t[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) t[k] = h ? tau[k].y : tau[k].x;
+                int kk;
+                const float ph = phi_any<MODE>(t, h ? sum8.y : sum8.x, kk);
+                const Normal n = finish_tail(!isnan(C.z[i + 1]), gu32[i], gv32[i], ph, kk == 0, c.a[i], b,
+                                             c.fx, c.fy);
+                nx[i] = n.x; ny[i] = n.y; nz[i] = n.z;
+            }
+            continue;
         }
         float2 phi;
         if (MODE == MEAN) {
@@ -220,7 +244,8 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     //      out-of-image taps are NaN, so the fast path already produced the canonical NaN ----
     const bool row_border = (v == 0) || (v == c.H - 1);
     special &= row_border ? 0u : ~colmask;
-    if (__any_sync(0xffffffffu, special != 0)) {
+    if (!GEN && __any_sync(0xffffffffu, special != 0)) {
+        if (c.fired && (threadIdx.x & 31) == 0) atomicAdd(c.fired, 1);
         // rare: skipped candidates, flat / tie, invalid samples -> exact per-pixel path
         // (re-reads the 3x3 from L1; bit-identical to tfn_pixel_kernel)
         for (int i = 0; i < 4; ++i) {
@@ -247,7 +272,44 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     }
 }
 
-template <int F, int MODE, bool DISP, int LAYOUT>
+// Rows [ys, y1) of one strip: prologue, then the rolling window down the strip.
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN>
+__device__ __forceinline__ void strip_rows(const StripCtx& c, float* out, long long HW, int layout,
+                                          unsigned colmask, int ys, int y1) {
+    Slot S0, S1, S2;
+    // prologue: rows ys-1 (S0), ys (S1) prepared; row ys+1 (S2) loaded
+    load_raw(S0, c, ys - 1);
+    load_raw(S1, c, ys);
+    load_raw(S2, c, ys + 1);
+    prepare<DISP, GEN>(S0, c);
+    prepare<DISP, GEN>(S1, c);
+    load_raw(S0, c, ys + 2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        S1.head[i] = grad_head<F>(Taps<F>::corners ? __dsub_rn(S0.w[i + 2], S0.w[i]) : 0.0,
+                                  __dsub_rn(S1.w[i + 2], S1.w[i]));
+        const float zc = S1.z[i + 1];
+        S1.rN[i] = pair_rcp<DISP>(S0.z[i + 1], zc);
+        S1.rNW[i] = pair_rcp<DISP>(S0.z[i], zc);
+        S1.rNE[i] = pair_rcp<DISP>(S0.z[i + 2], zc);
+    }
+    float vf = __int2float_rn(ys);      // exact row index as float (rows < 2^24)
+    for (int v = ys; v < y1; v += 3) {
+        row_step<F, MODE, DISP, LAYOUT, GEN>(S0, S1, S2, v, c, out, HW, layout, colmask, vf);
+        if (v + 1 >= y1) break;
+        row_step<F, MODE, DISP, LAYOUT, GEN>(S1, S2, S0, v + 1, c, out, HW, layout, colmask, vf + 1.0f);
+        if (v + 2 >= y1) break;
+        row_step<F, MODE, DISP, LAYOUT, GEN>(S2, S0, S1, v + 2, c, out, HW, layout, colmask, vf + 2.0f);
+        vf += 3.0f;
+    }
+}
+
+// KV (kernel variant): 0 fast path + exact per-pixel special path, 1 general (no special
+// path: skips, flat, ties and invalid taps resolved in registers; ~45 % more instructions
+// per pixel, but no divergent exact-path calls — the better choice when many row steps
+// contain special pixels: holes, salt dropout, integer-quantized depth).  The fast variant
+// counts its special row steps into p.fired (host-side AUTO selection, tfn_abi.cu).
+template <int F, int MODE, bool DISP, int LAYOUT, int KV>
 #ifdef TFN_STRIP_MAXNREG
 __global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(KernelArgs p) {
 #else
@@ -265,6 +327,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
     c.H = p.H; c.W = p.W;
     c.fx = p.fx; c.fy = p.fy;
     c.u0 = p.u0; c.v0 = p.v0;
+    c.fired = p.fired;
 
     // first item static, the rest claimed from a work counter (load balance: strips with
     // holes or sky cost more or less than others); static striding without a counter
@@ -292,32 +355,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
         }
         float* out = p.out + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm);
 
-        Slot S0, S1, S2;
-        // prologue: rows y0-1 (S0), y0 (S1) prepared; row y0+1 (S2) loaded
-        load_raw(S0, c, y0 - 1);
-        load_raw(S1, c, y0);
-        load_raw(S2, c, y0 + 1);
-        prepare<DISP>(S0, c);
-        prepare<DISP>(S1, c);
-        load_raw(S0, c, y0 + 2);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            S1.head[i] = grad_head<F>(Taps<F>::corners ? __dsub_rn(S0.w[i + 2], S0.w[i]) : 0.0,
-                                      __dsub_rn(S1.w[i + 2], S1.w[i]));
-            const float zc = S1.z[i + 1];
-            S1.rN[i] = pair_rcp<DISP>(S0.z[i + 1], zc);
-            S1.rNW[i] = pair_rcp<DISP>(S0.z[i], zc);
-            S1.rNE[i] = pair_rcp<DISP>(S0.z[i + 2], zc);
-        }
-        float vf = __int2float_rn(y0);      // exact row index as float (rows < 2^24)
-        for (int v = y0; v < y1; v += 3) {
-            row_step<F, MODE, DISP, LAYOUT>(S0, S1, S2, v, c, out, HW, p.layout, colmask, vf);
-            if (v + 1 >= y1) break;
-            row_step<F, MODE, DISP, LAYOUT>(S1, S2, S0, v + 1, c, out, HW, p.layout, colmask, vf + 1.0f);
-            if (v + 2 >= y1) break;
-            row_step<F, MODE, DISP, LAYOUT>(S2, S0, S1, v + 2, c, out, HW, p.layout, colmask, vf + 2.0f);
-            vf += 3.0f;
-        }
+        strip_rows<F, MODE, DISP, LAYOUT, KV == 1>(c, out, HW, p.layout, colmask, y0, y1);
         if (p.work) {
             int nxt = 0;
             if (lane == 0) nxt = atomicAdd(p.work, 1);

@@ -24,14 +24,14 @@ TFN_OK, TFN_ERR_INVALID_ARGUMENT, TFN_ERR_CONFIG, TFN_ERR_CUDA = 0, 1, 2, 3
 FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3}
 MODES = {"mean": 0, "median": 1}
 LAYOUTS = {"planar": 0, "packed": 1}
-KERNELS = {"auto": 0, "pixel": 1, "strip": 2}
+KERNELS = {"auto": 0, "pixel": 1, "strip": 2, "general": 3}
 OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_DYNAMIC = 0, 1, 2, 3
 
 # every symbol include/tfn.h declares (tests/test_abi.py checks the export table)
 ABI_SYMBOLS = (
     "tfn_create", "tfn_set_layout", "tfn_set_option", "tfn_estimate", "tfn_estimate_disparity",
     "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8", "tfn_destroy", "tfn_status_string",
-    "tfn_kernel_launches", "tfn_version", "tfn_debug_sol",
+    "tfn_kernel_launches", "tfn_version", "tfn_debug_sol", "tfn_auto_variant",
 )
 
 
@@ -68,6 +68,7 @@ def lib() -> ctypes.CDLL:
         L.tfn_debug_phi8.argtypes = [vp, ll, i, vp, vp, vp]
         L.tfn_debug_sol.argtypes = [vp, i, i, i, vp, vp]
         L.tfn_destroy.argtypes = [vp]
+        L.tfn_auto_variant.argtypes = [vp, ctypes.POINTER(i)]
         L.tfn_status_string.argtypes = [i]
         L.tfn_status_string.restype = ctypes.c_char_p
         L.tfn_kernel_launches.restype = ctypes.c_ulonglong
@@ -76,7 +77,8 @@ def lib() -> ctypes.CDLL:
             if f.restype is ctypes.c_int or name in ("tfn_create", "tfn_set_layout", "tfn_set_option",
                                                      "tfn_estimate", "tfn_estimate_disparity",
                                                      "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8",
-                                                     "tfn_destroy", "tfn_version", "tfn_debug_sol"):
+                                                     "tfn_destroy", "tfn_version", "tfn_debug_sol",
+                                                     "tfn_auto_variant"):
                 f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -155,6 +157,13 @@ def tfn_kernel_launches() -> int:
 
 def tfn_version() -> int:
     return int(lib().tfn_version())
+
+
+def tfn_auto_variant(h: int) -> int:
+    """The strip variant AUTO currently picks for handle h: 2 fast, 3 general."""
+    v = ctypes.c_int(0)
+    _check(lib().tfn_auto_variant(h, ctypes.byref(v)), "tfn_auto_variant")
+    return v.value
 
 
 # ----------------------------------------------------------------- tensor helpers

@@ -361,3 +361,66 @@ def test_full_size_config2_sampled(tfn):
                 tie = np.abs(np.sum(r[ok] * p, 1)) < 1e-6
                 a = np.where(tie, np.minimum(a, metrics.angular_error_deg(-gg[ok], r[ok])), a)
                 assert a.max() <= TOL_DEG, (fidx, a.max())
+
+
+# ------------------------------------------------------------------ general strip variant
+def _general_cases(cfg1, random8):
+    """(name, input, K, disparity?) covering skips, holes, invalid encodings, quantization,
+    flat / apex, borders and ragged sizes."""
+    rng = np.random.default_rng(11)
+    z8 = random8.depth.numpy()[:3].copy()
+    bad = np.array([0.0, -1.0, np.nan, np.inf, -np.inf, 1e-45, -0.0], np.float32)
+    sel = rng.random(z8.shape) < 0.15
+    z8[sel] = bad[rng.integers(0, len(bad), sel.sum())]
+    q = (np.round(random8.depth64.numpy()[:2] * 1000.0) / 1000.0).astype(np.float32)
+    holes = ts.render(ts.random_scenes(1, ts.K_1080, 1080, 1920, seed=7, holes=True, salt=0.01),
+                      ts.K_1080, 1080, 1920).depth.numpy()
+    flat = np.full((1, 64, 68), 2.5, np.float32)
+    K33 = ts.Intrinsics(200.0, 210.0, 130 / 2 - 0.3, 33 / 2 + 0.7)
+    small = ts.render(ts.random_scenes(2, K33, 33, 132, seed=3), K33, 33, 132).depth.numpy()
+    small[rng.random(small.shape) < 0.05] = 0.0
+    d = ts.depth_to_disparity(random8.depth64[:2], 500.0, 0.12).numpy()
+    return [("cfg1", cfg1.depth.numpy(), ts.K_VGA, False), ("invalid", z8, ts.K_VGA, False),
+            ("quantized", q, ts.K_VGA, False), ("holes1080", holes, ts.K_1080, False),
+            ("flat", flat, ts.K_VGA, False), ("small", small, K33, False),
+            ("disparity", d, ts.K_VGA, True)]
+
+
+def test_general_kernel_bitwise_vs_pixel(tfn, cfg1, random8):
+    """kernel=3 (no special path: skips, flat, ties, invalid taps all handled in registers)
+    is bit-identical to the per-pixel kernel on every hard case, and parity-green."""
+    for name, z, K, disp in _general_cases(cfg1, random8):
+        for f in FILTERS:
+            for m in MODES:
+                gg = run_gpu(tfn, z, K, f, m, disp=disp, kernel="general")
+                gp = run_gpu(tfn, z, K, f, m, disp=disp, kernel="pixel")
+                assert np.array_equal(gg.view(np.uint32), gp.view(np.uint32)), (name, f, m)
+                gk = run_gpu(tfn, z, K, f, m, disp=disp, kernel="general", layout="packed")
+                assert np.array_equal(gg.view(np.uint32), gk.view(np.uint32)), (name, f, m, "packed")
+    z = random8.depth.numpy()
+    for f in ("sobel", "fd"):
+        for m in MODES:
+            check(tfn, z, ts.K_VGA, f, m, kernel="general")
+
+
+def test_auto_variant_follows_the_special_rate(tfn, cfg1):
+    """AUTO starts on the fast strip kernel, moves to the general one on hole-heavy input
+    (config-4 style: ~98 % of row steps need the special path) and back on clean input;
+    the output is bit-identical whichever variant ran."""
+    from paper_2005_08165_b200 import tfn as T
+    sc = ts.random_scenes(2, ts.K_1080, 1080, 1920, seed=7, holes=True, salt=0.01)
+    holes = ts.render(sc, ts.K_1080, 1080, 1920).depth.cuda()
+    est = tfn.Estimator(ts.K_1080, "sobel", "median")
+    assert T.tfn_auto_variant(est.h) == 2
+    ref = run_gpu(tfn, holes.cpu().numpy(), ts.K_1080, "sobel", "median", kernel="pixel")
+    for _ in range(40):
+        out = est.estimate(holes)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    assert T.tfn_auto_variant(est.h) == 3
+    clean = cfg1.depth.reshape(1, 480, 640).repeat(4, 1, 1).cuda()
+    est2 = tfn.Estimator(ts.K_VGA, "sobel", "median")
+    for _ in range(40):
+        est2.estimate(clean)
+        torch.cuda.synchronize()
+    assert T.tfn_auto_variant(est2.h) == 2
