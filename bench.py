@@ -34,6 +34,7 @@ import tfn_scenes as ts  # noqa: E402
 
 METRIC = "Mpixel/s and 480×640 frames/s per B200 and at 2/4/8 GPUs; % HBM roofline"
 BYTES_PER_PX = 16  # 4 B fp32 sample read + 12 B fp32 normal written
+DEPTH_SCALE = 1e-3  # config 6: millimetre uint16 depth codes
 
 CONFIGS = {
     # id: (frames per rank, H, W, K, filter, mode, input, holes/salt, description)
@@ -48,6 +49,9 @@ CONFIGS = {
     5: dict(frames=65536, H=480, W=640, K=ts.K_VGA, filter="sobel", mode="median", disp=False, holes=False,
             desc="65536 x 480x640 streamed in 1024-frame chunks, sharded over ranks (configs[4])",
             scene="random", stream=True),
+    6: dict(frames=1024, H=480, W=640, K=ts.K_VGA, filter="sobel", mode="median", disp=False, holes=False,
+            desc="1024 x 480x640 uint16 millimetre depth codes -> half normals, Sobel + median "
+                 "(SURVEY §8(f) N1: 8 B/px)", scene="random", u16=True, out="f16"),
 }
 BASELINE_F = 500.0
 BASELINE_B = 0.12
@@ -63,6 +67,7 @@ def parse():
     ap.add_argument("--filter", default=None)
     ap.add_argument("--mode", default=None)
     ap.add_argument("--layout", default="planar", choices=["planar", "packed"])
+    ap.add_argument("--out", default=None, choices=["f32", "f16"], help="normal dtype (default: the config's)")
     ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
     ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel", "general"])
     ap.add_argument("--strip-h", type=int, default=0)
@@ -193,10 +198,26 @@ def make_frames(cfg, n, first, seed, device):
             del r
         depth = torch.cat(ds)
         gt = torch.cat(gs)
+        if cfg.get("u16"):
+            depth = to_codes(depth)
         return depth, gt
     if cfg["disp"]:
         depth = ts.depth_to_disparity(d64, BASELINE_F, BASELINE_B).expand(n, H, W).contiguous()
     return depth, gt
+
+
+def to_codes(depth: torch.Tensor) -> torch.Tensor:
+    """fp32 metres -> uint16 millimetre codes (0 = no return), as an RGB-D sensor delivers them"""
+    c = torch.round(depth * (1.0 / DEPTH_SCALE))
+    c = torch.where(torch.isfinite(c) & (c > 0), c, torch.zeros_like(c)).clamp(0, 65535)
+    return c.to(torch.int32).to(torch.uint16)
+
+
+def oracle_input(cfg, x: torch.Tensor) -> np.ndarray:
+    """what the oracle is fed: the samples themselves, or for codes the fp64 depths code x scale"""
+    if cfg.get("u16"):
+        return x.to(torch.int32).numpy().astype(np.float64) * DEPTH_SCALE
+    return x.numpy()
 
 
 # ------------------------------------------------------------------ reference arm (oracle)
@@ -211,7 +232,7 @@ def run_reference(args, cfg, ws, rank):
     # a bounded sample of the workload per step: `cores` frames (one per thread)
     n = cores
     depth, _ = make_frames(cfg, n, 0, args.seed, "cpu")
-    x = depth.numpy()
+    x = oracle_input(cfg, depth)
     kw = dict(disparity=cfg["disp"], f_tc=BASELINE_F * BASELINE_B)
     for _ in range(max(0, args.warmup)):
         oracle.estimate(x, cfg["K"], filt, mode, threads=cores, **kw)
@@ -247,12 +268,12 @@ def cpu_baseline(cfg, filt, mode, seconds, seed):
     d1, _ = make_frames(cfg, 1, 0, seed, "cpu")
     kw = dict(disparity=cfg["disp"], f_tc=BASELINE_F * BASELINE_B)
     t0 = time.perf_counter()
-    oracle.estimate(d1.numpy(), cfg["K"], filt, mode, **kw)
+    oracle.estimate(oracle_input(cfg, d1), cfg["K"], filt, mode, **kw)
     t1 = time.perf_counter() - t0
     n = int(max(cores, min(cfg["frames"], round(seconds * cores / max(t1, 1e-3)))))
     n = (n // cores) * cores or cores
     depth, _ = make_frames(cfg, n, 0, seed, "cpu")
-    x = depth.numpy()
+    x = oracle_input(cfg, depth)
     passes, t = 0, 0.0
     while t < seconds and passes < 64:           # repeat the same frames to ~`seconds` of wall time
         t0 = time.perf_counter()
@@ -296,19 +317,23 @@ def main():
     per_rank = last - first
     chunk = min(per_rank, 1024) if streaming_cfg else per_rank
 
+    out_dtype = args.out or cfg.get("out", "f32")
+    odt = torch.float16 if out_dtype == "f16" else torch.float32
+    in_b = 2 if cfg.get("u16") else 4
+    bytes_px = in_b + 3 * (2 if out_dtype == "f16" else 4)
     est = tfn.Estimator(K, filter=filt, nz_mode=mode, layout=args.layout, kernel=args.kernel,
-                        strip_h=args.strip_h, grid=args.grid, dynamic=not args.static)
+                        strip_h=args.strip_h, grid=args.grid, dynamic=not args.static, out_dtype=out_dtype)
     stream = torch.cuda.current_stream(dev)
 
     def launch(x, out):
         if cfg["disp"]:
             est.estimate_disparity(x, BASELINE_F * BASELINE_B, out=out, stream=stream)
         else:
-            est.estimate(x, out=out, stream=stream)
+            est.estimate(x, out=out, stream=stream, depth_scale=DEPTH_SCALE)
 
     x, gt = make_frames(cfg, chunk, first, args.seed, dev)
     out = torch.empty((chunk, 3, H, W) if args.layout == "planar" else (chunk, H, W, 3),
-                      dtype=torch.float32, device=dev)
+                      dtype=odt, device=dev)
     torch.cuda.synchronize()
     for _ in range(max(args.warmup, 3 if not args.profile else args.warmup)):
         launch(x, out)
@@ -373,12 +398,12 @@ def main():
     value = all_units / (total_ms_max / 1e3) / 1e6           # Mpixel/s whole job
     per_launch_ms = kernel_ms / steps
     px_per_launch = (chunk if not streaming_cfg else chunk) * H * W
-    achieved = BYTES_PER_PX * px_per_launch / (per_launch_ms / 1e3) / 1e9
+    achieved = bytes_px * px_per_launch / (per_launch_ms / 1e3) / 1e9
     peak, peak_kind = load_peaks()
 
     # a8 accuracy statistics vs analytic GT (off the timed region), NCCL all-reduce of int64
     if not streaming_cfg and not args.profile:
-        tfn.stats(out, gt, layout=args.layout, acc=acc, stream=stream)
+        tfn.stats(out if odt == torch.float32 else out.float(), gt, layout=args.layout, acc=acc, stream=stream)
     tdist.allreduce_stats(acc)                 # the only collective (NCCL, int64 SUM)
     st = acc.cpu().tolist()
     accuracy = None
@@ -389,7 +414,7 @@ def main():
     # (after the stats: it overwrites `out`) same-mix speed of light (4 B in + 12 B out per pixel, no arithmetic) for context
     sol = None
     if not args.profile and not streaming_cfg:
-        ok_sol = (H * W) % 4 == 0
+        ok_sol = (H * W) % 4 == 0 and bytes_px == BYTES_PER_PX
         if ok_sol:
             for _ in range(2):
                 tfn.debug_sol(x, out, stream=stream)
@@ -406,8 +431,8 @@ def main():
     e2e = None
     if not args.no_e2e and not args.profile and not streaming_cfg:
         hin = x.cpu().pin_memory()
-        hout = torch.empty(out.shape, dtype=torch.float32, pin_memory=True)
-        bf = BASELINE_F * BASELINE_B
+        hout = torch.empty(out.shape, dtype=odt, pin_memory=True)
+        bf = DEPTH_SCALE if cfg.get("u16") else BASELINE_F * BASELINE_B
         est.estimate_host(hin, is_disparity=cfg["disp"], baseline_times_f=bf, out=hout)
         if pg:
             pg.barrier()
@@ -422,7 +447,8 @@ def main():
             pg.all_reduce(tt, op=pg.ReduceOp.MAX)
         dt = float(tt.item())
         e2e = {"value": per_rank * H * W * args.e2e_steps * ws / dt / 1e6, "unit": "Mpixel/s",
-               "h2d_bytes_per_step": int(hin.numel() * 4), "d2h_bytes_per_step": int(hout.numel() * 4),
+               "h2d_bytes_per_step": int(hin.numel() * hin.element_size()),
+               "d2h_bytes_per_step": int(hout.numel() * hout.element_size()),
                "api": "tfn_estimate_host (pinned host buffers, chunked H2D/kernel/D2H on 2 streams)"}
         del hin, hout
 
@@ -436,18 +462,21 @@ def main():
             "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": ws, "steps": steps,
             "warmup": args.warmup, "ms_per_step": total_ms_max / steps, "higher_is_better": True,
             "scaling": "weak" if not streaming_cfg else "strong", "vs_baseline": None,
-            "dtype": "f32 (fp64 gradient path)", "data": "synthetic (seeded analytic ray-cast scenes)",
+            "dtype": "f32 (fp64 gradient path)" + (", u16 depth codes in" if cfg.get("u16") else "") +
+                     (", f16 normals out" if out_dtype == "f16" else ""),
+            "data": "synthetic (seeded analytic ray-cast scenes)",
             "config": {"workload": cfg["desc"], "filter": filt, "nz_mode": mode, "layout": args.layout,
-                       "input": "disparity" if cfg["disp"] else "depth", "frames_per_gpu": per_rank,
+                       "input": "disparity" if cfg["disp"] else ("depth u16 mm codes" if cfg.get("u16") else "depth"),
+                       "out_dtype": out_dtype, "frames_per_gpu": per_rank,
                        "H": H, "W": W, "fps": value * 1e6 / (H * W),
-                       "l2": "inputs (%.2f GB/GPU) larger than the 126 MB L2; no flush" % (chunk * H * W * 4 / 1e9),
+                       "l2": "inputs (%.2f GB/GPU) larger than the 126 MB L2; no flush" % (chunk * H * W * in_b / 1e9),
                        "parallelism": f"dp{ws} (frame batches sharded, no collective on the hot path)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "GB/launch (ncu dram read+write)",
-                         "algorithmic_GB_per_launch": BYTES_PER_PX * px_per_launch / 1e9,
+                         "algorithmic_GB_per_launch": bytes_px * px_per_launch / 1e9,
                          "sol_same_mix_GBps": sol, "frac_of_sol": (achieved / sol) if sol else None,
                          "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                         "kernel": "tfn_strip_kernel", "bytes_per_px": BYTES_PER_PX,
+                         "kernel": "tfn_strip_kernel", "bytes_per_px": bytes_px,
                          "px_per_launch": px_per_launch, "launch_ms": per_launch_ms},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
             "cpu_baseline": cpu, "accuracy_vs_gt": accuracy,

@@ -17,9 +17,12 @@
  * median, orientation tie, ...) are DESIGN.md §3 (Q1-Q19); they are identical to
  * the fp64 oracle's (oracle/tfn_oracle.c).
  *
- * Data layout.  Inputs are contiguous fp32 [batch, H, W] row-major.  A sample is
- * VALID iff it is finite and >= FLT_MIN (zero, negative, NaN, Inf and fp32
- * subnormals mean "no measurement").  Outputs are fp32 unit normals:
+ * Data layout.  Inputs are contiguous fp32 [batch, H, W] row-major (or, for
+ * tfn_estimate_u16, uint16 depth codes: Z = code x depth_scale, code 0 = no
+ * measurement — SURVEY §8(f) N1).  A fp32 sample is VALID iff it is finite and
+ * >= FLT_MIN (zero, negative, NaN, Inf and fp32 subnormals mean "no measurement").
+ * Outputs are unit normals, fp32 (default) or IEEE half (TFN_OPT_OUT_DTYPE =
+ * TFN_OUT_F16: each component the fp32 result rounded to nearest; NaN stays NaN):
  *   TFN_LAYOUT_PLANAR  [batch, 3, H, W]  (n_x plane, n_y plane, n_z plane)
  *   TFN_LAYOUT_PACKED  [batch, H, W, 3]
  * An output pixel is VALID iff it is not on the 1-pixel image border, its centre
@@ -29,8 +32,9 @@
  *
  * Ownership.  The caller owns every buffer.  Device pointers must be cudaMalloc'd
  * (or torch) memory on the current device; inputs and outputs must not overlap.
- * 16-byte-aligned buffers with W % 4 == 0 take the strip kernel (the fast path);
- * anything else (>= 4-byte aligned) takes the per-pixel kernel, same results.
+ * With W % 4 == 0 and buffers aligned to 4 elements (16 B fp32, 8 B uint16 / half)
+ * the strip kernel runs (the fast path); anything else (element-aligned) takes the
+ * per-pixel kernel, same results.
  * A handle holds only its parameters (plus, for tfn_estimate_host, a lazily
  * allocated device workspace guarded by a mutex); set options before the first
  * estimate.  Device calls are asynchronous on `stream` (a cudaStream_t passed as
@@ -57,6 +61,7 @@ typedef enum {
 typedef enum { TFN_FILTER_FD = 0, TFN_FILTER_SOBEL = 1, TFN_FILTER_SCHARR = 2, TFN_FILTER_PREWITT = 3 } tfn_filter;
 typedef enum { TFN_NZ_MEAN = 0, TFN_NZ_MEDIAN = 1 } tfn_nz_mode;
 typedef enum { TFN_LAYOUT_PLANAR = 0, TFN_LAYOUT_PACKED = 1 } tfn_layout;
+typedef enum { TFN_OUT_F32 = 0, TFN_OUT_F16 = 1 } tfn_out_dtype;
 
 /* Options for tfn_set_option (tuning / testing; defaults are the production path) */
 typedef enum {
@@ -64,7 +69,8 @@ typedef enum {
                             /* 3 general strip kernel (same results; no special path: for holes / quantized)  */
     TFN_OPT_STRIP_H = 1,    /* rows per warp strip, 0 = auto (>= 4)                                        */
     TFN_OPT_GRID = 2,       /* CTAs of the strip kernel, 0 = auto (resident CTAs x SMs)                    */
-    TFN_OPT_DYNAMIC = 3     /* 1 (default): strips claimed from a per-call work counter; 0: static stride  */
+    TFN_OPT_DYNAMIC = 3,    /* 1 (default): strips claimed from a per-call work counter; 0: static stride  */
+    TFN_OPT_OUT_DTYPE = 4   /* tfn_out_dtype of the normals every estimate call writes (default F32)        */
 } tfn_option;
 
 /* Pinhole intrinsics in pixels (Eq. 13): u = column, v = row, 0-based, pixel
@@ -86,25 +92,39 @@ int tfn_set_layout(tfn_handle h, int layout);
 int tfn_set_option(tfn_handle h, int option, long long value);
 
 /* 3F2N from depth (Eq. 13-18).  depth: device fp32 [batch,H,W] in metres
- * (any positive unit); out_normals: device fp32, 3*batch*H*W floats in the
- * handle's layout.  Asynchronous on stream. */
+ * (any positive unit); out_normals: device, 3*batch*H*W components of the handle's
+ * output dtype (fp32 or half) in the handle's layout.  Asynchronous on stream. */
 int tfn_estimate(tfn_handle h, const float* depth, int batch, int H, int W,
-                 void* stream, float* out_normals);
+                 void* stream, void* out_normals);
+
+/* 3F2N from integer depth codes (e.g. millimetre depth from RGB-D
+ * sensors): depth_codes device uint16 [batch,H,W], Z = code * depth_scale, code 0 =
+ * no measurement.  depth_scale > 0 and finite (CONFIG otherwise); it cancels from the
+ * normal direction (Appendix A.4) and is only validated.  Same output as
+ * tfn_estimate on the fp32 depths code * depth_scale up to rounding (<= 1e-3 deg; the
+ * oracle parity bar), bit-identical to tfn_estimate on the fp32 values (float)code.
+ * Quantized depth makes dZ == 0 common, so the general strip variant runs. */
+int tfn_estimate_u16(tfn_handle h, const unsigned short* depth_codes, double depth_scale, int batch, int H,
+                     int W, void* stream, void* out_normals);
 
 /* 3F2N from disparity (Eq. 19-21): z = f t_c / d.  Requires fx == fy
  * (CONFIG otherwise).  baseline_times_f = f * t_c > 0 and finite (CONFIG otherwise);
  * it cancels from the normal direction and is only validated. */
 int tfn_estimate_disparity(tfn_handle h, const float* disparity, double baseline_times_f,
-                           int batch, int H, int W, void* stream, float* out_normals);
+                           int batch, int H, int W, void* stream, void* out_normals);
 
 /* End-to-end from HOST memory: copies host_in (fp32 [batch,H,W], depth or
  * disparity) to the device in chunks, runs the same kernel, copies the normals back
- * to host_out (3*batch*H*W floats), overlapping H2D / kernel / D2H on two internal
- * streams.  Pinned host memory gives full overlap.  Blocking: returns when host_out
- * is complete (or on the first error).  `stream` orders the work after prior work
- * on that stream. */
+ * to host_out (3*batch*H*W components of the output dtype), overlapping H2D / kernel /
+ * D2H on two internal streams.  Pinned host memory gives full overlap.  Blocking:
+ * returns when host_out is complete (or on the first error).  `stream` orders the
+ * work after prior work on that stream. */
 int tfn_estimate_host(tfn_handle h, const float* host_in, int is_disparity, double baseline_times_f,
-                      int batch, int H, int W, float* host_out, void* stream);
+                      int batch, int H, int W, void* host_out, void* stream);
+
+/* tfn_estimate_host for uint16 depth codes (see tfn_estimate_u16). */
+int tfn_estimate_host_u16(tfn_handle h, const unsigned short* host_codes, double depth_scale, int batch, int H,
+                          int W, void* host_out, void* stream);
 
 /* angular-error statistics (Eq. 22-24) of est (device,
  * layout `layout`) against gt (device, planar [batch,3,H,W], NaN = invalid), ADDED

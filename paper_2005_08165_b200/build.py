@@ -12,8 +12,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtfn.so")
-SOURCES = ["tfn_abi.cu", "tfn_kernels.cu", "tfn_stats.cu"]
-HEADERS = ["tfn_device.cuh", "tfn_kernels.h", os.path.join("..", "..", "include", "tfn.h")]
+SOURCES = ["tfn_abi.cu", "tfn_kernels.cu", "tfn_stats.cu", "tfn_strip_fd.cu", "tfn_strip_sobel.cu",
+           "tfn_strip_scharr.cu", "tfn_strip_prewitt.cu"]
+HEADERS = ["tfn_device.cuh", "tfn_kernels.h", "tfn_strip.cuh", "tfn_strip_inst.cuh",
+           os.path.join("..", "..", "include", "tfn.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-fvisibility=hidden",
               "--expt-relaxed-constexpr", "-Xptxas", "-v"]

@@ -19,10 +19,11 @@ namespace {
 std::atomic<unsigned long long> g_launches{0};
 
 struct Workspace {
-    float* in[2] = {nullptr, nullptr};
-    float* out[2] = {nullptr, nullptr};
+    void* in[2] = {nullptr, nullptr};
+    void* out[2] = {nullptr, nullptr};
     size_t frames = 0;        // capacity in frames of one chunk
-    size_t frame_px = 0;
+    size_t frame_in = 0;      // bytes per frame the buffers were sized for
+    size_t frame_out = 0;
     cudaStream_t s[2] = {nullptr, nullptr};
     cudaEvent_t start = nullptr;
 };
@@ -34,13 +35,15 @@ struct tfn_ctx {
     int filter;
     int mode;
     int layout = TFN_LAYOUT_PLANAR;
+    int out_f16 = 0;                     // TFN_OPT_OUT_DTYPE
     int kernel = tfn::TFN_KERNEL_AUTO;
     int strip_h = 0;
     int grid = 0;
     int dynamic = 1;
     int device = 0;
     int sms = 148;
-    int strip_ctas_per_sm[2][2] = {{0, 0}, {0, 0}};   // [fast, general][depth, disparity]
+    int strip_ctas_per_sm[2][2] = {{0, 0}, {0, 0}};   // fp32 input: [fast, general][depth, disparity]
+    int strip_ctas_u16 = 0;                           // uint16 depth codes (general variant)
     std::mutex ws_mu;
     Workspace ws;
     int* work = nullptr;                 // ring of per-call {work, fired} counter pairs
@@ -89,22 +92,30 @@ bool overlap(const void* a, size_t na, const void* b, size_t nb) {
     return x < y + nb && y < x + na;
 }
 
-int validate(tfn_handle h, const float* in, int batch, int H, int W, const float* out) {
+// bytes per sample in / per normal component out
+size_t in_bytes(int in_u16) { return in_u16 ? 2 : 4; }
+size_t out_bytes(const tfn_ctx* h) { return h->out_f16 ? 2 : 4; }
+
+int validate(tfn_handle h, const void* in, int in_u16, int batch, int H, int W, const void* out) {
     if (!h) return TFN_ERR_INVALID_ARGUMENT;
     if (batch < 0 || H <= 0 || W <= 0) return TFN_ERR_INVALID_ARGUMENT;
     if (batch == 0) return TFN_OK;
     if (!in || !out) return TFN_ERR_INVALID_ARGUMENT;
     const unsigned long long px = (unsigned long long)batch * (unsigned long long)H * (unsigned long long)W;
     if (px > (1ull << 60) / 12) return TFN_ERR_INVALID_ARGUMENT;
-    if (((uintptr_t)in & 3) || ((uintptr_t)out & 3)) return TFN_ERR_INVALID_ARGUMENT;
-    if (overlap(in, px * 4, out, px * 12)) return TFN_ERR_INVALID_ARGUMENT;
+    const size_t ib = in_bytes(in_u16), ob = out_bytes(h);
+    if (((uintptr_t)in & (ib - 1)) || ((uintptr_t)out & (ob - 1))) return TFN_ERR_INVALID_ARGUMENT;
+    if (overlap(in, px * ib, out, px * 3 * ob)) return TFN_ERR_INVALID_ARGUMENT;
     return TFN_OK;
 }
 
-int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaStream_t st, float* out) {
+int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, int W, cudaStream_t st,
+        void* out) {
     tfn::KernelArgs a;
     a.in = in;
     a.out = out;
+    a.in_u16 = in_u16;
+    a.out_f16 = h->out_f16;
     a.B = batch;
     a.H = H;
     a.W = W;
@@ -113,15 +124,19 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
     a.u0 = (float)h->K.u0;
     a.v0 = (float)h->K.v0;
     a.layout = h->layout;
-    // strip kernel: 16-B vectors, and (frame, strip-row, strip-col) items indexed in 32 bits
+    // strip kernel: 4-sample vectors in and 4-component vectors out (16 B fp32, 8 B for
+    // uint16 / half), and (frame, strip-row, strip-col) items indexed in 32 bits
     const long long max_items = (long long)((W + 127) / 128) * ((H + 3) / 4) * (long long)batch;
-    const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & 15) == 0) && (((uintptr_t)out & 15) == 0) &&
+    const uintptr_t in_al = 4 * in_bytes(in_u16) - 1, out_al = 4 * out_bytes(h) - 1;
+    const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & in_al) == 0) && (((uintptr_t)out & out_al) == 0) &&
                           max_items < (1LL << 31);
     int kernel = h->kernel;
     bool probe = false;
     if (kernel == tfn::TFN_KERNEL_AUTO) {
         if (!strip_ok) {
             kernel = tfn::TFN_KERNEL_PIXEL;
+        } else if (in_u16) {
+            kernel = tfn::TFN_KERNEL_STRIP_GENERAL;     // the only strip variant built for codes
         } else {
             std::lock_guard<std::mutex> lk(h->auto_mu);
             if (h->fb_pending && cudaEventQuery(h->fb_ev) == cudaSuccess) {
@@ -138,13 +153,14 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
                     (h->auto_general || (n % TFN_AUTO_PROBE_FAST) == 0);
         }
     }
+    if (in_u16 && kernel == tfn::TFN_KERNEL_STRIP) kernel = tfn::TFN_KERNEL_STRIP_GENERAL;   // same results
     const bool strip = (kernel == tfn::TFN_KERNEL_STRIP || kernel == tfn::TFN_KERNEL_STRIP_GENERAL);
     if (strip && !strip_ok) return TFN_ERR_INVALID_ARGUMENT;
     const int gen = (kernel == tfn::TFN_KERNEL_STRIP_GENERAL) ? 1 : 0;
     int grid = 0;
     if (strip) {
-        const long long resident_warps =
-            (long long)h->sms * h->strip_ctas_per_sm[gen][disp] * (TFN_STRIP_THREADS / 32);
+        const int ctas_sm = in_u16 ? h->strip_ctas_u16 : h->strip_ctas_per_sm[gen][disp];
+        const long long resident_warps = (long long)h->sms * ctas_sm * (TFN_STRIP_THREADS / 32);
         int sh = h->strip_h;
         const long long sx_n = (W + 127) / 128;
         if (sh <= 0) {
@@ -164,7 +180,7 @@ int run(tfn_handle h, const float* in, bool disp, int batch, int H, int W, cudaS
             a.fired = probe ? ctr + 1 : nullptr;
         }
         const long long items = sx_n * ((H + sh - 1) / sh) * (long long)batch;
-        long long ctas = h->grid > 0 ? h->grid : (long long)h->sms * h->strip_ctas_per_sm[gen][disp];
+        long long ctas = h->grid > 0 ? h->grid : (long long)h->sms * ctas_sm;
         const long long need = (items + (TFN_STRIP_THREADS / 32) - 1) / (TFN_STRIP_THREADS / 32);
         if (ctas > need) ctas = need;
         if (ctas < 1) ctas = 1;
@@ -210,9 +226,11 @@ TFN_API int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_han
     for (int g = 0; g < 2; ++g)
         for (int d = 0; d < 2; ++d) {
             int& n = h->strip_ctas_per_sm[g][d];
-            n = tfn::strip_occupancy(filter, nz_mode, d != 0, g);
+            n = tfn::strip_occupancy(filter, nz_mode, d != 0, g, 0);
             if (n <= 0) n = 1;
         }
+    h->strip_ctas_u16 = tfn::strip_occupancy(filter, nz_mode, false, 1, 1);
+    if (h->strip_ctas_u16 <= 0) h->strip_ctas_u16 = 1;
     if (cudaMalloc(&h->work, 2 * TFN_WORK_RING * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         h->work = nullptr;                // static scheduling (and the fast AUTO choice) still work
@@ -251,47 +269,59 @@ TFN_API int tfn_set_option(tfn_handle h, int option, long long value) {
     case TFN_OPT_DYNAMIC:
         h->dynamic = value ? 1 : 0;
         return TFN_OK;
+    case TFN_OPT_OUT_DTYPE:
+        if (value != TFN_OUT_F32 && value != TFN_OUT_F16) return TFN_ERR_INVALID_ARGUMENT;
+        h->out_f16 = (int)value;
+        return TFN_OK;
     default:
         return TFN_ERR_INVALID_ARGUMENT;
     }
 }
 
 TFN_API int tfn_estimate(tfn_handle h, const float* depth, int batch, int H, int W, void* stream,
-                         float* out_normals) {
-    int st = validate(h, depth, batch, H, W, out_normals);
+                         void* out_normals) {
+    int st = validate(h, depth, 0, batch, H, W, out_normals);
     if (st != TFN_OK || batch == 0) return st;
-    return run(h, depth, false, batch, H, W, (cudaStream_t)stream, out_normals);
+    return run(h, depth, 0, false, batch, H, W, (cudaStream_t)stream, out_normals);
+}
+
+TFN_API int tfn_estimate_u16(tfn_handle h, const unsigned short* depth_codes, double depth_scale, int batch, int H,
+                             int W, void* stream, void* out_normals) {
+    if (!h) return TFN_ERR_INVALID_ARGUMENT;
+    if (!is_fin(depth_scale) || depth_scale <= 0) return TFN_ERR_CONFIG;   // validated; cancels (A.4)
+    int st = validate(h, depth_codes, 1, batch, H, W, out_normals);
+    if (st != TFN_OK || batch == 0) return st;
+    return run(h, depth_codes, 1, false, batch, H, W, (cudaStream_t)stream, out_normals);
 }
 
 TFN_API int tfn_estimate_disparity(tfn_handle h, const float* disparity, double baseline_times_f,
-                                   int batch, int H, int W, void* stream, float* out_normals) {
+                                   int batch, int H, int W, void* stream, void* out_normals) {
     if (!h) return TFN_ERR_INVALID_ARGUMENT;
     if (h->K.fx != h->K.fy) return TFN_ERR_CONFIG;                       // Eq. 19: one f
     if (!is_fin(baseline_times_f) || baseline_times_f <= 0) return TFN_ERR_CONFIG;
-    int st = validate(h, disparity, batch, H, W, out_normals);
+    int st = validate(h, disparity, 0, batch, H, W, out_normals);
     if (st != TFN_OK || batch == 0) return st;
-    return run(h, disparity, true, batch, H, W, (cudaStream_t)stream, out_normals);
+    return run(h, disparity, 0, true, batch, H, W, (cudaStream_t)stream, out_normals);
 }
 
-TFN_API int tfn_estimate_host(tfn_handle h, const float* host_in, int is_disparity, double baseline_times_f,
-                              int batch, int H, int W, float* host_out, void* stream) {
-    if (!h) return TFN_ERR_INVALID_ARGUMENT;
-    if (is_disparity) {
-        if (h->K.fx != h->K.fy) return TFN_ERR_CONFIG;
-        if (!is_fin(baseline_times_f) || baseline_times_f <= 0) return TFN_ERR_CONFIG;
-    }
+namespace {
+
+// the pipelined host-buffer path shared by tfn_estimate_host / tfn_estimate_host_u16:
+// ~48 MB chunks alternate between two streams (H2D copy, kernel, D2H copy)
+int host_run(tfn_handle h, const void* host_in, int in_u16, bool disp, int batch, int H, int W, void* host_out,
+             void* stream) {
     if (batch < 0 || H <= 0 || W <= 0) return TFN_ERR_INVALID_ARGUMENT;
     if (batch == 0) return TFN_OK;
     if (!host_in || !host_out) return TFN_ERR_INVALID_ARGUMENT;
     const size_t fpx = (size_t)H * (size_t)W;
     if ((unsigned long long)batch * fpx > (1ull << 60) / 12) return TFN_ERR_INVALID_ARGUMENT;
+    const size_t fin = fpx * in_bytes(in_u16), fout = fpx * 3 * out_bytes(h);
     std::lock_guard<std::mutex> lock(h->ws_mu);
     Workspace& ws = h->ws;
-    // ~48 MB of input per chunk: large enough to saturate PCIe, small enough to pipeline
-    size_t chunk = (48u << 20) / (fpx * 4);
+    size_t chunk = (48u << 20) / fin;
     if (chunk < 1) chunk = 1;
     if (chunk > (size_t)batch) chunk = batch;
-    if (ws.frames < chunk || ws.frame_px != fpx) {
+    if (ws.frames < chunk || ws.frame_in < fin || ws.frame_out < fout) {
         for (int i = 0; i < 2; ++i) {
             if (ws.in[i]) cudaFree(ws.in[i]);
             if (ws.out[i]) cudaFree(ws.out[i]);
@@ -299,14 +329,14 @@ TFN_API int tfn_estimate_host(tfn_handle h, const float* host_in, int is_dispari
         }
         ws.frames = 0;
         for (int i = 0; i < 2; ++i) {
-            if (cudaMalloc(&ws.in[i], chunk * fpx * 4) != cudaSuccess ||
-                cudaMalloc(&ws.out[i], chunk * fpx * 12) != cudaSuccess) {
+            if (cudaMalloc(&ws.in[i], chunk * fin) != cudaSuccess || cudaMalloc(&ws.out[i], chunk * fout) != cudaSuccess) {
                 cudaGetLastError();
                 return TFN_ERR_CUDA;
             }
         }
         ws.frames = chunk;
-        ws.frame_px = fpx;
+        ws.frame_in = fin;
+        ws.frame_out = fout;
     }
     if (!ws.s[0]) {
         for (int i = 0; i < 2; ++i)
@@ -320,16 +350,18 @@ TFN_API int tfn_estimate_host(tfn_handle h, const float* host_in, int is_dispari
     int rc = TFN_OK;
     size_t done = 0;
     int k = 0;
+    const char* hin = static_cast<const char*>(host_in);
+    char* hout = static_cast<char*>(host_out);
     while (done < (size_t)batch) {
         const size_t n = ((size_t)batch - done < chunk) ? (size_t)batch - done : chunk;
         cudaStream_t s = ws.s[k & 1];
-        if (cudaMemcpyAsync(ws.in[k & 1], host_in + done * fpx, n * fpx * 4, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+        if (cudaMemcpyAsync(ws.in[k & 1], hin + done * fin, n * fin, cudaMemcpyHostToDevice, s) != cudaSuccess) {
             rc = TFN_ERR_CUDA;
             break;
         }
-        rc = run(h, ws.in[k & 1], is_disparity != 0, (int)n, H, W, s, ws.out[k & 1]);
+        rc = run(h, ws.in[k & 1], in_u16, disp, (int)n, H, W, s, ws.out[k & 1]);
         if (rc != TFN_OK) break;
-        if (cudaMemcpyAsync(host_out + done * fpx * 3, ws.out[k & 1], n * fpx * 12, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+        if (cudaMemcpyAsync(hout + done * fout, ws.out[k & 1], n * fout, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
             rc = TFN_ERR_CUDA;
             break;
         }
@@ -339,6 +371,25 @@ TFN_API int tfn_estimate_host(tfn_handle h, const float* host_in, int is_dispari
     for (int i = 0; i < 2; ++i)
         if (cudaStreamSynchronize(ws.s[i]) != cudaSuccess) rc = TFN_ERR_CUDA;
     return rc;
+}
+
+}  // namespace
+
+TFN_API int tfn_estimate_host(tfn_handle h, const float* host_in, int is_disparity, double baseline_times_f,
+                              int batch, int H, int W, void* host_out, void* stream) {
+    if (!h) return TFN_ERR_INVALID_ARGUMENT;
+    if (is_disparity) {
+        if (h->K.fx != h->K.fy) return TFN_ERR_CONFIG;
+        if (!is_fin(baseline_times_f) || baseline_times_f <= 0) return TFN_ERR_CONFIG;
+    }
+    return host_run(h, host_in, 0, is_disparity != 0, batch, H, W, host_out, stream);
+}
+
+TFN_API int tfn_estimate_host_u16(tfn_handle h, const unsigned short* host_codes, double depth_scale, int batch, int H,
+                                  int W, void* host_out, void* stream) {
+    if (!h) return TFN_ERR_INVALID_ARGUMENT;
+    if (!is_fin(depth_scale) || depth_scale <= 0) return TFN_ERR_CONFIG;
+    return host_run(h, host_codes, 1, false, batch, H, W, host_out, stream);
 }
 
 TFN_API int tfn_stats(const float* est, const float* gt, int batch, int H, int W, int layout, void* stream,

@@ -1,5 +1,6 @@
 // tfn_kernels.h — internal launch interface between the C ABI (tfn_abi.cu) and the
-// kernels (tfn_kernels.cu, tfn_stats.cu).  Not part of the public ABI (include/tfn.h).
+// kernels (tfn_kernels.cu + tfn_strip_<filter>.cu, tfn_stats.cu).  Not part of the public
+// ABI (include/tfn.h).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -14,9 +15,13 @@ namespace tfn {
 
 enum KernelId { TFN_KERNEL_AUTO = 0, TFN_KERNEL_PIXEL = 1, TFN_KERNEL_STRIP = 2, TFN_KERNEL_STRIP_GENERAL = 3 };
 
+enum InDtype { TFN_IN_F32 = 0, TFN_IN_U16 = 1 };
+
 struct KernelArgs {
-    const float* in;     // [B,H,W] depth or disparity
-    float* out;          // [B,3,H,W] (layout 0) or [B,H,W,3] (layout 1)
+    const void* in;      // [B,H,W] depth or disparity: fp32, or uint16 depth codes (in_u16)
+    void* out;           // [B,3,H,W] (layout 0) or [B,H,W,3] (layout 1): fp32, or half (out_f16)
+    int in_u16;
+    int out_f16;
     long long B;
     int H, W;
     float fx, fy;        // n' = (fx g_u, fy g_v, n_z)   (Eq. 18)
@@ -31,7 +36,13 @@ cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, in
                         int grid_strip, cudaStream_t st);
 
 // resident CTAs per SM of the strip kernel variant (occupancy query)
-int strip_occupancy(int filter, int mode, bool disp, int variant);   // 0 fast, 1 general
+int strip_occupancy(int filter, int mode, bool disp, int variant, int in_u16);   // variant 0 fast, 1 general
+
+// per-filter strip instantiations (tfn_strip_<filter>.cu, compiled in parallel)
+template <int F>
+cudaError_t launch_strip(const KernelArgs& a, int mode, bool disp, int variant, int grid, cudaStream_t st);
+template <int F>
+int occupancy_strip(int mode, bool disp, int variant, int in_u16);
 
 // a8: angular-error statistics vs ground truth (off the timed path)
 cudaError_t launch_stats(const float* est, const float* gt, long long B, int H, int W,

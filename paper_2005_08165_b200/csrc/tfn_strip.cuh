@@ -31,9 +31,10 @@ struct Slot {
     float rN[4], rNW[4], rNE[4];   // pair reciprocals of the N / NW / NE neighbours (pairs owned by the row above)
 };
 
+template <class T>
 struct StripCtx {
-    const float* img;  // frame base
-    const float* pm;   // frame base + clamped column of the lane's float4
+    const T* img;      // frame base (fp32 samples or uint16 depth codes)
+    const T* pm;       // frame base + clamped column of the lane's 4-vector
     int cm;            // clamped first column of the lane
     float u0;
     int H, W;
@@ -41,12 +42,18 @@ struct StripCtx {
     float fx, fy;
     float a[4];        // u - u0 of the 4 columns
     int* fired;        // AUTO probe: += 1 per row step that needed the special path
+    bool f16;          // normals stored as IEEE half (N1), else fp32
     float v0;
 };
 
-// row v of the lane's window: one LDG.128 + two halo LDG.32 at immediate offsets,
-// predicated off outside the image (never an out-of-bounds address)
-__device__ __forceinline__ void load_raw(Slot& s, const StripCtx& c, int v) {
+// uint16 code -> float, exactly, without a conversion instruction: 2^23 + code has the code
+// in its low mantissa bits (PRMT builds the word, one FADD removes the 2^23)
+__device__ __forceinline__ float code_lo(unsigned x) { return __uint_as_float(__byte_perm(x, 0x4B00u, 0x5410)) - 8388608.0f; }
+__device__ __forceinline__ float code_hi(unsigned x) { return __uint_as_float(__byte_perm(x, 0x4B00u, 0x5432)) - 8388608.0f; }
+
+// row v of the lane's window: one LDG.128 (fp32) or LDG.64 (uint16) + two halo loads at
+// immediate offsets, predicated off outside the image (never an out-of-bounds address)
+__device__ __forceinline__ void load_raw(Slot& s, const StripCtx<float>& c, int v) {
     s.rok = (v >= 0) && (v < c.H);
     const float* row = c.pm + v * c.W;
     if (s.rok) {
@@ -55,6 +62,16 @@ __device__ __forceinline__ void load_raw(Slot& s, const StripCtx& c, int v) {
     }
     if (s.rok && c.okl) s.raw[0] = __ldg(row - 1);
     if (s.rok && c.okr) s.raw[5] = __ldg(row + 4);
+}
+__device__ __forceinline__ void load_raw(Slot& s, const StripCtx<unsigned short>& c, int v) {
+    s.rok = (v >= 0) && (v < c.H);
+    const unsigned short* row = c.pm + v * c.W;
+    if (s.rok) {
+        const uint2 m = __ldg(reinterpret_cast<const uint2*>(row));
+        s.raw[1] = code_lo(m.x); s.raw[2] = code_hi(m.x); s.raw[3] = code_lo(m.y); s.raw[4] = code_hi(m.y);
+    }
+    if (s.rok && c.okl) s.raw[0] = code_lo(__ldg(row - 1));
+    if (s.rok && c.okr) s.raw[5] = code_lo(__ldg(row + 4));
 }
 
 // Q5 for the fast path: valid iff finite and >= FLT_MIN (rejects 0, negatives, NaN,
@@ -66,8 +83,8 @@ __device__ __forceinline__ float sanitize_fast(float z, bool ok) {
     return good ? z : __int_as_float(0x7fffffff);
 }
 
-template <bool DISP, bool GEN>
-__device__ __forceinline__ void prepare(Slot& s, const StripCtx& c) {
+template <bool DISP, bool GEN, class T>
+__device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
     s.z[0] = sanitize_fast<DISP>(s.raw[0], s.rok && c.okl);
 #pragma unroll
     for (int j = 1; j <= 4; ++j) s.z[j] = sanitize_fast<DISP>(s.raw[j], s.rok && c.okm);
@@ -90,13 +107,20 @@ __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b
 __device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
     __stcs(reinterpret_cast<float4*>(p), make_float4(a, b, c, d));
 }
+__device__ __forceinline__ unsigned h2(float a, float b) {      // RN to half, NaN stays NaN
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const unsigned*>(&h);
+}
+__device__ __forceinline__ void st4h(void* p, float a, float b, float c, float d) {
+    __stcs(reinterpret_cast<uint2*>(p), make_uint2(h2(a, b), h2(c, d)));
+}
 
 // One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw holds row v+2 in
 // flight), C = slot(v) (C.raw receives row v+3), N = slot(v+1) (N.raw loaded; the rest
 // computed here).
-template <int F, int MODE, bool DISP, int LAYOUT, bool GEN>
-__device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx& c,
-                                         float* __restrict__ out, long long HW, int layout,
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T>
+__device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
+                                         char* __restrict__ out, long long HW, int layout,
                                          unsigned colmask, float vf) {
     load_raw(C, c, v + 3);                       // prefetch three rows ahead (C.raw is free)
     prepare<DISP, GEN>(N, c);
@@ -256,25 +280,37 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
             }
         }
     }
-    // ---- store (16-B aligned: W % 4 == 0, c0 % 4 == 0) ----
+    // ---- store (16-B / 8-B aligned: W % 4 == 0, c0 % 4 == 0) ----
     if (c.okm) {
-        float* o = out + v * c.W;
-        if (LAYOUT == 0) {
-            st4(o, nx[0], nx[1], nx[2], nx[3]);
-            st4(o + HW, ny[0], ny[1], ny[2], ny[3]);
-            st4(o + 2 * HW, nz[0], nz[1], nz[2], nz[3]);
+        if (!c.f16) {
+            float* o = reinterpret_cast<float*>(out) + v * c.W * (LAYOUT == 0 ? 1 : 3);
+            if (LAYOUT == 0) {
+                st4(o, nx[0], nx[1], nx[2], nx[3]);
+                st4(o + HW, ny[0], ny[1], ny[2], ny[3]);
+                st4(o + 2 * HW, nz[0], nz[1], nz[2], nz[3]);
+            } else {
+                st4(o, nx[0], ny[0], nz[0], nx[1]);
+                st4(o + 4, ny[1], nz[1], nx[2], ny[2]);
+                st4(o + 8, nz[2], nx[3], ny[3], nz[3]);
+            }
         } else {
-            o += v * c.W * 2;     // packed: 3 floats per pixel
-            st4(o, nx[0], ny[0], nz[0], nx[1]);
-            st4(o + 4, ny[1], nz[1], nx[2], ny[2]);
-            st4(o + 8, nz[2], nx[3], ny[3], nz[3]);
+            __half* o = reinterpret_cast<__half*>(out) + v * c.W * (LAYOUT == 0 ? 1 : 3);
+            if (LAYOUT == 0) {
+                st4h(o, nx[0], nx[1], nx[2], nx[3]);
+                st4h(o + HW, ny[0], ny[1], ny[2], ny[3]);
+                st4h(o + 2 * HW, nz[0], nz[1], nz[2], nz[3]);
+            } else {
+                st4h(o, nx[0], ny[0], nz[0], nx[1]);
+                st4h(o + 4, ny[1], nz[1], nx[2], ny[2]);
+                st4h(o + 8, nz[2], nx[3], ny[3], nz[3]);
+            }
         }
     }
 }
 
 // Rows [ys, y1) of one strip: prologue, then the rolling window down the strip.
-template <int F, int MODE, bool DISP, int LAYOUT, bool GEN>
-__device__ __forceinline__ void strip_rows(const StripCtx& c, float* out, long long HW, int layout,
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T>
+__device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long long HW, int layout,
                                           unsigned colmask, int ys, int y1) {
     Slot S0, S1, S2;
     // prologue: rows ys-1 (S0), ys (S1) prepared; row ys+1 (S2) loaded
@@ -295,11 +331,11 @@ __device__ __forceinline__ void strip_rows(const StripCtx& c, float* out, long l
     }
     float vf = __int2float_rn(ys);      // exact row index as float (rows < 2^24)
     for (int v = ys; v < y1; v += 3) {
-        row_step<F, MODE, DISP, LAYOUT, GEN>(S0, S1, S2, v, c, out, HW, layout, colmask, vf);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T>(S0, S1, S2, v, c, out, HW, layout, colmask, vf);
         if (v + 1 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN>(S1, S2, S0, v + 1, c, out, HW, layout, colmask, vf + 1.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T>(S1, S2, S0, v + 1, c, out, HW, layout, colmask, vf + 1.0f);
         if (v + 2 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN>(S2, S0, S1, v + 2, c, out, HW, layout, colmask, vf + 2.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T>(S2, S0, S1, v + 2, c, out, HW, layout, colmask, vf + 2.0f);
         vf += 3.0f;
     }
 }
@@ -309,7 +345,7 @@ __device__ __forceinline__ void strip_rows(const StripCtx& c, float* out, long l
 // per pixel, but no divergent exact-path calls — the better choice when many row steps
 // contain special pixels: holes, salt dropout, integer-quantized depth).  The fast variant
 // counts its special row steps into p.fired (host-side AUTO selection, tfn_abi.cu).
-template <int F, int MODE, bool DISP, int LAYOUT, int KV>
+template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T>
 #ifdef TFN_STRIP_MAXNREG
 __global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(KernelArgs p) {
 #else
@@ -323,11 +359,13 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
     const int items = sx_n * sy_n * (int)p.B;          // < 2^31, checked by the host
     const long long HW = (long long)p.H * p.W;
 
-    StripCtx c;
+    StripCtx<T> c;
     c.H = p.H; c.W = p.W;
     c.fx = p.fx; c.fy = p.fy;
     c.u0 = p.u0; c.v0 = p.v0;
     c.fired = p.fired;
+    c.f16 = p.out_f16 != 0;
+    const int es = c.f16 ? 2 : 4;          // bytes per output component
 
     // first item static, the rest claimed from a work counter (load balance: strips with
     // holes or sky cost more or less than others); static striding without a counter
@@ -343,7 +381,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
         c.okl = c.okm && c0 >= 1;
         c.okr = c0 + 4 < p.W;
         c.cm = min(c0, p.W - 4);
-        c.img = p.in + fb * HW;
+        c.img = reinterpret_cast<const T*>(p.in) + fb * HW;
         c.pm = c.img + c.cm;
 #pragma unroll
         for (int i = 0; i < 4; ++i) c.a[i] = __fsub_rn(__int2float_rn(c0 + i), c.u0);   // a = u - u0
@@ -353,9 +391,9 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
             if (c0 == 0) colmask |= 1u;
             if (c0 + 3 == p.W - 1) colmask |= 8u;
         }
-        float* out = p.out + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm);
+        char* out = reinterpret_cast<char*>(p.out) + es * (fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm));
 
-        strip_rows<F, MODE, DISP, LAYOUT, KV == 1>(c, out, HW, p.layout, colmask, y0, y1);
+        strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T>(c, out, HW, p.layout, colmask, y0, y1);
         if (p.work) {
             int nxt = 0;
             if (lane == 0) nxt = atomicAdd(p.work, 1);

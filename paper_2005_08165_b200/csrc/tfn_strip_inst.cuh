@@ -1,0 +1,64 @@
+// tfn_strip_inst.cuh — launch / occupancy wrappers of the strip kernel for ONE gradient
+// filter F; each tfn_strip_<filter>.cu instantiates them, so the four filters compile in
+// parallel.  Instantiated set: fp32 input x {depth, disparity} x {mean, median} x
+// {planar, packed} x {fast, general}; uint16 depth codes (N1) x {mean, median} x
+// {planar, packed} x {general} (integer-quantized depth makes dZ = 0 common, so the
+// fast variant's special path would run on most row steps).
+#pragma once
+#include "tfn_device.cuh"
+#include "tfn_kernels.h"
+#include "tfn_strip.cuh"
+
+namespace tfn {
+
+template <int F, int MODE, bool DISP, int KV, class T>
+static cudaError_t launch_l(const KernelArgs& a, int grid, cudaStream_t st) {
+    if (a.layout == 0) tfn_strip_kernel<F, MODE, DISP, 0, KV, T><<<grid, TFN_STRIP_THREADS, 0, st>>>(a);
+    else tfn_strip_kernel<F, MODE, DISP, 1, KV, T><<<grid, TFN_STRIP_THREADS, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int F, int MODE>
+static cudaError_t launch_m(const KernelArgs& a, bool disp, int variant, int grid, cudaStream_t st) {
+    if (a.in_u16) {
+        if (disp) return cudaErrorInvalidValue;
+        return launch_l<F, MODE, false, 1, unsigned short>(a, grid, st);
+    }
+    if (disp) return variant ? launch_l<F, MODE, true, 1, float>(a, grid, st) : launch_l<F, MODE, true, 0, float>(a, grid, st);
+    return variant ? launch_l<F, MODE, false, 1, float>(a, grid, st) : launch_l<F, MODE, false, 0, float>(a, grid, st);
+}
+
+template <int F>
+cudaError_t launch_strip(const KernelArgs& a, int mode, bool disp, int variant, int grid, cudaStream_t st) {
+    return mode == MEAN ? launch_m<F, MEAN>(a, disp, variant, grid, st) : launch_m<F, MEDIAN>(a, disp, variant, grid, st);
+}
+
+template <class K>
+static int occ(K kernel) {
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, TFN_STRIP_THREADS, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return 1;
+    }
+    return n;
+}
+
+template <int F, int MODE>
+static int occ_m(bool disp, int variant, int in_u16) {
+    if (in_u16) return occ(tfn_strip_kernel<F, MODE, false, 0, 1, unsigned short>);
+    if (disp) return variant ? occ(tfn_strip_kernel<F, MODE, true, 0, 1, float>) : occ(tfn_strip_kernel<F, MODE, true, 0, 0, float>);
+    return variant ? occ(tfn_strip_kernel<F, MODE, false, 0, 1, float>) : occ(tfn_strip_kernel<F, MODE, false, 0, 0, float>);
+}
+
+template <int F>
+int occupancy_strip(int mode, bool disp, int variant, int in_u16) {
+    return mode == MEAN ? occ_m<F, MEAN>(disp, variant, in_u16) : occ_m<F, MEDIAN>(disp, variant, in_u16);
+}
+
+}  // namespace tfn
+
+#define TFN_INSTANTIATE_STRIP(F)                                                                        \
+    namespace tfn {                                                                                    \
+    template cudaError_t launch_strip<F>(const KernelArgs&, int, bool, int, int, cudaStream_t);       \
+    template int occupancy_strip<F>(int, bool, int, int);                                              \
+    }

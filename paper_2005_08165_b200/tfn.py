@@ -25,13 +25,15 @@ FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3}
 MODES = {"mean": 0, "median": 1}
 LAYOUTS = {"planar": 0, "packed": 1}
 KERNELS = {"auto": 0, "pixel": 1, "strip": 2, "general": 3}
-OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_DYNAMIC = 0, 1, 2, 3
+OUT_DTYPES = {"f32": 0, "f16": 1}
+OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_DYNAMIC, OPT_OUT_DTYPE = 0, 1, 2, 3, 4
 
 # every symbol include/tfn.h declares (tests/test_abi.py checks the export table)
 ABI_SYMBOLS = (
     "tfn_create", "tfn_set_layout", "tfn_set_option", "tfn_estimate", "tfn_estimate_disparity",
     "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8", "tfn_destroy", "tfn_status_string",
-    "tfn_kernel_launches", "tfn_version", "tfn_debug_sol", "tfn_auto_variant",
+    "tfn_kernel_launches", "tfn_version", "tfn_debug_sol", "tfn_auto_variant", "tfn_estimate_u16",
+    "tfn_estimate_host_u16",
 )
 
 
@@ -64,6 +66,8 @@ def lib() -> ctypes.CDLL:
         L.tfn_estimate.argtypes = [vp, vp, i, i, i, vp, vp]
         L.tfn_estimate_disparity.argtypes = [vp, vp, d, i, i, i, vp, vp]
         L.tfn_estimate_host.argtypes = [vp, vp, i, d, i, i, i, vp, vp]
+        L.tfn_estimate_u16.argtypes = [vp, vp, d, i, i, i, vp, vp]
+        L.tfn_estimate_host_u16.argtypes = [vp, vp, d, i, i, i, vp, vp]
         L.tfn_stats.argtypes = [vp, vp, i, i, i, i, vp, vp]
         L.tfn_debug_phi8.argtypes = [vp, ll, i, vp, vp, vp]
         L.tfn_debug_sol.argtypes = [vp, i, i, i, vp, vp]
@@ -78,7 +82,8 @@ def lib() -> ctypes.CDLL:
                                                      "tfn_estimate", "tfn_estimate_disparity",
                                                      "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8",
                                                      "tfn_destroy", "tfn_version", "tfn_debug_sol",
-                                                     "tfn_auto_variant"):
+                                                     "tfn_auto_variant", "tfn_estimate_u16",
+                                                     "tfn_estimate_host_u16"):
                 f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -115,6 +120,16 @@ def tfn_set_option(h: int, option: int, value: int) -> None:
 
 def tfn_estimate(h: int, depth_ptr: int, batch: int, H: int, W: int, stream: int, out_ptr: int) -> int:
     return lib().tfn_estimate(h, depth_ptr, batch, H, W, stream, out_ptr)
+
+
+def tfn_estimate_u16(h: int, codes_ptr: int, depth_scale: float, batch: int, H: int, W: int, stream: int,
+                     out_ptr: int) -> int:
+    return lib().tfn_estimate_u16(h, codes_ptr, float(depth_scale), batch, H, W, stream, out_ptr)
+
+
+def tfn_estimate_host_u16(h: int, host_codes: int, depth_scale: float, batch: int, H: int, W: int,
+                          host_out: int, stream: int) -> int:
+    return lib().tfn_estimate_host_u16(h, host_codes, float(depth_scale), batch, H, W, host_out, stream)
 
 
 def tfn_estimate_disparity(h: int, disp_ptr: int, baseline_times_f: float, batch: int, H: int, W: int,
@@ -172,9 +187,9 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
     return int(s.cuda_stream)
 
 
-def _need(t: torch.Tensor, name: str, device: bool = True):
-    if t.dtype != torch.float32 or not t.is_contiguous():
-        raise TfnError(TFN_ERR_INVALID_ARGUMENT, f"{name} must be a contiguous float32 tensor")
+def _need(t: torch.Tensor, name: str, device: bool = True, dtype=torch.float32):
+    if t.dtype != dtype or not t.is_contiguous():
+        raise TfnError(TFN_ERR_INVALID_ARGUMENT, f"{name} must be a contiguous {dtype} tensor")
     if device and not t.is_cuda:
         raise TfnError(TFN_ERR_INVALID_ARGUMENT, f"{name} must be a CUDA tensor")
 
@@ -191,29 +206,41 @@ class Estimator:
     """One tfn handle: intrinsics K=(fx,fy,u0,v0), gradient kernel, Phi, layout."""
 
     def __init__(self, K, filter: str = "sobel", nz_mode: str = "median", layout: str = "planar",
-                 kernel: str = "auto", strip_h: int = 0, grid: int = 0, dynamic: bool = True):
+                 kernel: str = "auto", strip_h: int = 0, grid: int = 0, dynamic: bool = True,
+                 out_dtype: str = "f32"):
         self.K = K.as_tuple() if hasattr(K, "as_tuple") else tuple(float(x) for x in K)
         self.filter, self.nz_mode, self.layout = filter, nz_mode, layout
+        self.out_dtype = out_dtype
+        self._odt = torch.float16 if out_dtype == "f16" else torch.float32
         self.h = tfn_create(self.K, FILTERS[filter], MODES[nz_mode])
         tfn_set_layout(self.h, LAYOUTS[layout])
         tfn_set_option(self.h, OPT_KERNEL, KERNELS[kernel])
         tfn_set_option(self.h, OPT_STRIP_H, strip_h)
         tfn_set_option(self.h, OPT_GRID, grid)
         tfn_set_option(self.h, OPT_DYNAMIC, int(dynamic))
+        tfn_set_option(self.h, OPT_OUT_DTYPE, OUT_DTYPES[out_dtype])
 
     def _out(self, B, H, W, like: torch.Tensor, out):
         shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
         if out is None:
-            out = torch.empty(shape, dtype=torch.float32, device=like.device)
-        _need(out, "out", device=like.is_cuda)
+            out = torch.empty(shape, dtype=self._odt, device=like.device)
+        _need(out, "out", device=like.is_cuda, dtype=self._odt)
         if out.numel() != 3 * B * H * W:
             raise TfnError(TFN_ERR_INVALID_ARGUMENT, "out has the wrong size")
         return out
 
     def estimate(self, depth: torch.Tensor, out: Optional[torch.Tensor] = None,
-                 stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
-        _need(depth, "depth")
+                 stream: Optional[torch.cuda.Stream] = None, depth_scale: float = 1e-3) -> torch.Tensor:
+        """depth: CUDA fp32 [B,H,W] / [H,W], or uint16 depth codes (Z = code * depth_scale;
+        the scale is validated and cancels)."""
         B, H, W = _bhw(depth)
+        if depth.dtype == torch.uint16:
+            _need(depth, "depth", dtype=torch.uint16)
+            out = self._out(B, H, W, depth, out)
+            _check(tfn_estimate_u16(self.h, depth.data_ptr(), depth_scale, B, H, W, _stream_ptr(stream),
+                                    out.data_ptr()), "tfn_estimate_u16")
+            return out
+        _need(depth, "depth")
         out = self._out(B, H, W, depth, out)
         _check(tfn_estimate(self.h, depth.data_ptr(), B, H, W, _stream_ptr(stream), out.data_ptr()),
                "tfn_estimate")
@@ -232,16 +259,26 @@ class Estimator:
     def estimate_host(self, host_in: torch.Tensor, is_disparity: bool = False, baseline_times_f: float = 1.0,
                       out: Optional[torch.Tensor] = None,
                       stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
-        """Host buffers in and out (pinned for full overlap); blocking."""
-        _need(host_in, "host_in", device=False)
+        """Host buffers in and out (pinned for full overlap); blocking.  host_in fp32 (depth or
+        disparity) or uint16 depth codes (baseline_times_f is then the depth scale)."""
+        u16 = host_in.dtype == torch.uint16
+        _need(host_in, "host_in", device=False, dtype=torch.uint16 if u16 else torch.float32)
         if host_in.is_cuda:
             raise TfnError(TFN_ERR_INVALID_ARGUMENT, "host_in must be a CPU tensor")
         B, H, W = _bhw(host_in)
         if out is None:
             shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
-            out = torch.empty(shape, dtype=torch.float32, pin_memory=True)
-        _check(tfn_estimate_host(self.h, host_in.data_ptr(), int(is_disparity), baseline_times_f, B, H, W,
-                                 out.data_ptr(), _stream_ptr(stream)), "tfn_estimate_host")
+            out = torch.empty(shape, dtype=self._odt, pin_memory=True)
+        _need(out, "out", device=False, dtype=self._odt)
+        if out.numel() != 3 * B * H * W:
+            raise TfnError(TFN_ERR_INVALID_ARGUMENT, "out has the wrong size")
+        if u16:
+            _check(tfn_estimate_host_u16(self.h, host_in.data_ptr(), baseline_times_f if baseline_times_f != 1.0
+                                         else 1e-3, B, H, W, out.data_ptr(), _stream_ptr(stream)),
+                   "tfn_estimate_host_u16")
+        else:
+            _check(tfn_estimate_host(self.h, host_in.data_ptr(), int(is_disparity), baseline_times_f, B, H, W,
+                                     out.data_ptr(), _stream_ptr(stream)), "tfn_estimate_host")
         return out
 
     def close(self):
