@@ -49,6 +49,9 @@ CONFIGS = {
     5: dict(frames=65536, H=480, W=640, K=ts.K_VGA, filter="sobel", mode="median", disp=False, holes=False,
             desc="65536 x 480x640 streamed in 1024-frame chunks, sharded over ranks (configs[4])",
             scene="random", stream=True),
+    7: dict(frames=1024, H=480, W=640, K=ts.K_VGA, filter="fd", mode="median", disp=False, holes=False,
+            desc="1024 x 480x640 depth + Gaussian noise sigma = 0.3 % of mean depth (S:374 medium), FD + median "
+                 "(SURVEY §8(f) N2)", scene="random", noise="medium"),
     6: dict(frames=1024, H=480, W=640, K=ts.K_VGA, filter="sobel", mode="median", disp=False, holes=False,
             desc="1024 x 480x640 uint16 millimetre depth codes -> half normals, Sobel + median "
                  "(SURVEY §8(f) N1: 8 B/px)", scene="random", u16=True, out="f16"),
@@ -198,6 +201,8 @@ def make_frames(cfg, n, first, seed, device):
             del r
         depth = torch.cat(ds)
         gt = torch.cat(gs)
+        if cfg.get("noise"):
+            depth = ts.add_gaussian_noise(depth, ts.NOISE_PRESETS[cfg["noise"]], seed=seed, first_frame=first)
         if cfg.get("u16"):
             depth = to_codes(depth)
         return depth, gt

@@ -58,6 +58,7 @@ def lib():
         Kp = ctypes.POINTER(_K)
         L.orc_valid_sample.argtypes = [ctypes.c_double]; L.orc_valid_sample.restype = ctypes.c_int
         L.orc_backproject.argtypes = [Kp, ctypes.c_double, ctypes.c_double, ctypes.c_double, dp]
+        L.orc_backproject_image.argtypes = [Kp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
         L.orc_inverse_depth.argtypes = [ctypes.c_double]; L.orc_inverse_depth.restype = ctypes.c_double
         L.orc_disparity_to_depth.argtypes = [ctypes.c_double, ctypes.c_double]
         L.orc_disparity_to_depth.restype = ctypes.c_double
@@ -121,6 +122,19 @@ def backproject(K, u, v, z) -> np.ndarray:
     k = _kstruct(K)
     lib().orc_backproject(ctypes.byref(k), float(u), float(v), float(z), _dp(p))
     return p
+
+
+def backproject_image(depth: np.ndarray, K) -> np.ndarray:
+    """fp64 point cloud [B,3,H,W] of fp64 depth [B,H,W] (Eq. 13 per pixel,
+    NaN where the sample is invalid, Q5)."""
+    z = np.ascontiguousarray(depth, dtype=np.float64)
+    if z.ndim == 2:
+        z = z[None]
+    B, H, W = z.shape
+    out = np.empty((B, 3, H, W), dtype=np.float64)
+    k = _kstruct(K)
+    lib().orc_backproject_image(ctypes.byref(k), _dp(z), B, H, W, _dp(out))
+    return out
 
 
 def inverse_depth(z: float) -> float:

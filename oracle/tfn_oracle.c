@@ -66,6 +66,25 @@ ORC_EXPORT void orc_backproject(const orc_intrinsics* K, double u, double v, dou
     p[2] = z;
 }
 
+/* ---- the point cloud of a depth image — Eq. 13 at every pixel,
+ *      NaN for an invalid sample (Q5).  z: fp64 [B,H,W] depth; out: planar [B,3,H,W]. ---- */
+ORC_EXPORT void orc_backproject_image(const orc_intrinsics* K, const double* z, int B, int H, int W,
+                                      double* out)
+{
+    const size_t hw = (size_t)H * W;
+    for (int b = 0; b < B; ++b)
+        for (int v = 0; v < H; ++v)
+            for (int u = 0; u < W; ++u) {
+                const size_t i = (size_t)v * W + u;
+                double* o = out + (size_t)b * 3 * hw + i;
+                const double zz = z[(size_t)b * hw + i];
+                if (!orc_valid_sample(zz)) { o[0] = o[hw] = o[2 * hw] = NAN; continue; }
+                double p[3];
+                orc_backproject(K, (double)u, (double)v, zz, p);
+                o[0] = p[0]; o[hw] = p[1]; o[2 * hw] = p[2];
+            }
+}
+
 /* ---- P:197 inverse depth; Eq. 19 disparity -> depth -------------------------- */
 ORC_EXPORT double orc_inverse_depth(double z) { return 1.0 / z; }
 ORC_EXPORT double orc_disparity_to_depth(double f_times_tc, double d) { return f_times_tc / d; }

@@ -424,3 +424,29 @@ def test_auto_variant_follows_the_special_rate(tfn, cfg1):
         est2.estimate(clean)
         torch.cuda.synchronize()
     assert T.tfn_auto_variant(est2.h) == 2
+
+
+# ------------------------------------------------------------------ N2: noisy depth
+@pytest.mark.parametrize("level", ["low", "high"])
+def test_noisy_depth_parity(tfn, random8, level):
+    """Gaussian depth noise (S:374 presets) — parity, and the fast, general
+    and per-pixel kernels agree bit for bit on it."""
+    z = ts.add_gaussian_noise(random8.depth[:3], ts.NOISE_PRESETS[level], seed=11).numpy()
+    for f in ("fd", "sobel"):
+        for m in MODES:
+            g, _ = check(tfn, z, ts.K_VGA, f, m)
+            for kernel in ("strip", "general", "pixel"):
+                gk = run_gpu(tfn, z, ts.K_VGA, f, m, kernel=kernel)
+                assert np.array_equal(g.view(np.uint32), gk.view(np.uint32)), (level, f, m, kernel)
+
+
+def test_noise_median_beats_mean(tfn, random8):
+    """the method property behind Table VII / P:795: under depth noise the median Phi has a
+    lower average angular error than the mean (checked through the a8 stats kernel)"""
+    z = ts.add_gaussian_noise(random8.depth, ts.NOISE_PRESETS["medium"], seed=3).cuda()
+    gt = random8.gt.cuda()
+    aae = {}
+    for m in MODES:
+        acc = tfn.stats(tfn.Estimator(ts.K_VGA, "fd", m).estimate(z), gt).cpu().numpy()
+        aae[m] = acc[0] / 1e6 / acc[1]
+    assert aae["median"] < aae["mean"], aae

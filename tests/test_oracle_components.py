@@ -146,3 +146,38 @@ def test_pgp_monotone():
     psi = rng.uniform(0, 180, size=1000)
     vals = [metrics.pgp(psi, phi) for phi in np.linspace(0, 180, 50)]
     assert all(b >= a for a, b in zip(vals, vals[1:])) and vals[-1] == 1.0
+
+
+def test_backproject_image_pins():
+    """N3 oracle: every valid pixel's point satisfies Eq. 13's closed form X/Z = (u-u0)/fx,
+    Y/Z = (v-v0)/fy and, for a rendered plane, lies on that plane (n . p = n . q within
+    1e-9 m); invalid samples give NaN; the SPEC example point is reproduced."""
+    import oracle
+    import tfn_scenes as ts
+    K = ts.Intrinsics(510.0, 490.0, 31.7, 22.3)
+    n, q = np.array([0.3, -0.2, -1.0]), np.array([0.0, 0.0, 3.0])
+    r = ts.render(ts.plane_scene(tuple(n), tuple(q)), K, 48, 64, keep_depth64=True)
+    z = r.depth64.numpy().copy()
+    z[0, 5, 7] = 0.0
+    z[0, 9, 9] = np.nan
+    p = oracle.backproject_image(z, K)
+    assert p.shape == (1, 3, 48, 64)
+    assert np.isnan(p[0, :, 5, 7]).all() and np.isnan(p[0, :, 9, 9]).all()
+    ok = np.isfinite(z[0]) & (z[0] >= np.finfo(np.float32).tiny)
+    assert np.isnan(p[0, 0][~ok]).all()
+    vv, uu = np.nonzero(ok)
+    X, Y, Z = p[0, 0][ok], p[0, 1][ok], p[0, 2][ok]
+    assert np.array_equal(Z, z[0][ok])
+    assert np.allclose(X / Z, (uu - K.u0) / K.fx, rtol=0, atol=1e-12)
+    assert np.allclose(Y / Z, (vv - K.v0) / K.fy, rtol=0, atol=1e-12)
+    nn = n / np.linalg.norm(n)
+    assert np.abs(nn[0] * X + nn[1] * Y + nn[2] * Z - nn @ q).max() < 1e-9
+def test_backproject_image_spec_examples(golden):
+    """the SPEC back-projection examples through the image routine"""
+    import oracle
+    for ex in golden["backproject"]:
+        u, v, zval = ex["uvz"]
+        z = np.zeros((1, v + 1, u + 1))
+        z[0, v, u] = zval
+        p = oracle.backproject_image(z, tuple(ex["K"]))
+        assert np.allclose(p[0, :, v, u], ex["p"], rtol=0, atol=1e-12), ex["cite"]

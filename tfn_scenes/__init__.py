@@ -301,3 +301,32 @@ def depth_to_disparity(depth64_or_32: torch.Tensor, f: float, baseline: float) -
     fb = float(f) * float(baseline)
     d = torch.where(z > 0, fb / torch.where(z > 0, z, torch.ones_like(z)), torch.zeros_like(z))
     return d.to(torch.float32)
+
+
+# ----------------------------------------------------------------------------------
+# noise-robustness workload (PAPER.md supplement P:829-831, Table VII
+# P:706-758; SPEC S:357-366 add_gaussian_noise, S:374 presets)
+NOISE_PRESETS = {"low": 0.001, "medium": 0.003, "high": 0.01}   # sigma / mean valid depth
+
+
+def add_gaussian_noise(depth: torch.Tensor, sigma_rel: float, seed: int = 0, first_frame: int = 0) -> torch.Tensor:
+    """z' = z + sigma * N(0,1) on valid pixels (z > 0, finite), sigma = sigma_rel x the frame's
+    mean valid depth; pixels pushed to z' <= 0 become invalid (0).  Deterministic per
+    (seed, global frame id, pixel): counter-based uniforms (hash_uniform, integer ops)
+    -> Box-Muller in fp64.  No 3F2N arithmetic.  CPU and GPU agree to the last few ulps
+    of log/cos (not bit for bit): tests feed both sides the same host-generated frames."""
+    if sigma_rel == 0:
+        return depth.clone()
+    F = depth.shape[0]
+    npix = depth[0].numel()
+    dev = depth.device
+    ids = torch.arange(first_frame, first_frame + F, dtype=torch.int64)
+    u1 = hash_uniform(seed * 2 + 1, ids, npix, dev)
+    u2 = hash_uniform(seed * 2 + 2, ids, npix, dev)
+    g = torch.sqrt(-2.0 * torch.log1p(-u1)) * torch.cos((2.0 * math.pi) * u2)    # N(0,1), fp64
+    z = depth.reshape(F, npix).to(torch.float64)
+    valid = torch.isfinite(z) & (z > 0)
+    mean = torch.where(valid, z, torch.zeros_like(z)).sum(1) / valid.sum(1).clamp(min=1)
+    zn = z + (sigma_rel * mean)[:, None] * g
+    zn = torch.where(valid & (zn > 0), zn, torch.zeros_like(zn))
+    return zn.to(torch.float32).reshape(depth.shape)
