@@ -122,6 +122,19 @@ int tfn_estimate_disparity(tfn_handle h, const float* disparity, double baseline
 int tfn_estimate_host(tfn_handle h, const float* host_in, int is_disparity, double baseline_times_f,
                       int batch, int H, int W, void* host_out, void* stream);
 
+/* normals AND the point cloud in one pass (the downstream consumers:
+ * registration / SLAM).  input_kind (tfn_input_kind): fp32 depth
+ * (Z = scale * sample), fp32 disparity (Z = scale / d, scale = f * t_c, needs fx == fy),
+ * or uint16 depth codes (Z = scale * code).  scale > 0 and finite (CONFIG otherwise).
+ * out_normals as for tfn_estimate (same bits); out_points: device fp32, 3*batch*H*W
+ * floats in the handle's layout, p = Z (  (u-u0)/fx, (v-v0)/fy, 1 ) (Eq. 13), each
+ * coordinate rounded as fl(fl(a * Z) * fl(1/fx)) (<= 3 ulp of the fp64 value); NaN where
+ * the sample is invalid (the point needs no neighbours: border pixels get points).
+ * out_points must not overlap the other buffers; 16-B aligned for the strip kernel. */
+typedef enum { TFN_INPUT_DEPTH_F32 = 0, TFN_INPUT_DISPARITY_F32 = 1, TFN_INPUT_DEPTH_U16 = 2 } tfn_input_kind;
+int tfn_estimate_points(tfn_handle h, const void* input, int input_kind, double scale, int batch, int H, int W,
+                        void* stream, void* out_normals, float* out_points);
+
 /* tfn_estimate_host for uint16 depth codes (see tfn_estimate_u16). */
 int tfn_estimate_host_u16(tfn_handle h, const unsigned short* host_codes, double depth_scale, int batch, int H,
                           int W, void* host_out, void* stream);

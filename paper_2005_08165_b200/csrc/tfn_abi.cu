@@ -110,12 +110,16 @@ int validate(tfn_handle h, const void* in, int in_u16, int batch, int H, int W, 
 }
 
 int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, int W, cudaStream_t st,
-        void* out) {
+        void* out, float* pts = nullptr, double pscale = 1.0) {
     tfn::KernelArgs a;
     a.in = in;
     a.out = out;
     a.in_u16 = in_u16;
     a.out_f16 = h->out_f16;
+    a.pts = pts;
+    a.pscale = (float)pscale;
+    a.ifx = (float)(1.0 / h->K.fx);
+    a.ify = (float)(1.0 / h->K.fy);
     a.B = batch;
     a.H = H;
     a.W = W;
@@ -129,14 +133,14 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
     const long long max_items = (long long)((W + 127) / 128) * ((H + 3) / 4) * (long long)batch;
     const uintptr_t in_al = 4 * in_bytes(in_u16) - 1, out_al = 4 * out_bytes(h) - 1;
     const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & in_al) == 0) && (((uintptr_t)out & out_al) == 0) &&
-                          max_items < (1LL << 31);
+                          (((uintptr_t)pts & 15) == 0) && max_items < (1LL << 31);
     int kernel = h->kernel;
     bool probe = false;
     if (kernel == tfn::TFN_KERNEL_AUTO) {
         if (!strip_ok) {
             kernel = tfn::TFN_KERNEL_PIXEL;
-        } else if (in_u16) {
-            kernel = tfn::TFN_KERNEL_STRIP_GENERAL;     // the only strip variant built for codes
+        } else if (in_u16 || h->out_f16 || pts) {
+            kernel = tfn::TFN_KERNEL_STRIP_GENERAL;     // the only strip variant built for these
         } else {
             std::lock_guard<std::mutex> lk(h->auto_mu);
             if (h->fb_pending && cudaEventQuery(h->fb_ev) == cudaSuccess) {
@@ -153,7 +157,9 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
                     (h->auto_general || (n % TFN_AUTO_PROBE_FAST) == 0);
         }
     }
-    if (in_u16 && kernel == tfn::TFN_KERNEL_STRIP) kernel = tfn::TFN_KERNEL_STRIP_GENERAL;   // same results
+    // the fast strip variant is built for fp32 in / fp32 normals only; the general one has the
+    // same results (bit for bit) and runs everything else
+    if ((in_u16 || h->out_f16 || pts) && kernel == tfn::TFN_KERNEL_STRIP) kernel = tfn::TFN_KERNEL_STRIP_GENERAL;
     const bool strip = (kernel == tfn::TFN_KERNEL_STRIP || kernel == tfn::TFN_KERNEL_STRIP_GENERAL);
     if (strip && !strip_ok) return TFN_ERR_INVALID_ARGUMENT;
     const int gen = (kernel == tfn::TFN_KERNEL_STRIP_GENERAL) ? 1 : 0;
@@ -302,6 +308,26 @@ TFN_API int tfn_estimate_disparity(tfn_handle h, const float* disparity, double 
     int st = validate(h, disparity, 0, batch, H, W, out_normals);
     if (st != TFN_OK || batch == 0) return st;
     return run(h, disparity, 0, true, batch, H, W, (cudaStream_t)stream, out_normals);
+}
+
+TFN_API int tfn_estimate_points(tfn_handle h, const void* input, int input_kind, double scale, int batch, int H,
+                                int W, void* stream, void* out_normals, float* out_points) {
+    if (!h) return TFN_ERR_INVALID_ARGUMENT;
+    if (input_kind != TFN_INPUT_DEPTH_F32 && input_kind != TFN_INPUT_DISPARITY_F32 &&
+        input_kind != TFN_INPUT_DEPTH_U16)
+        return TFN_ERR_INVALID_ARGUMENT;
+    if (!is_fin(scale) || scale <= 0) return TFN_ERR_CONFIG;
+    const bool disp = input_kind == TFN_INPUT_DISPARITY_F32;
+    if (disp && h->K.fx != h->K.fy) return TFN_ERR_CONFIG;
+    const int u16 = input_kind == TFN_INPUT_DEPTH_U16 ? 1 : 0;
+    int st = validate(h, input, u16, batch, H, W, out_normals);
+    if (st != TFN_OK || batch == 0) return st;
+    if (!out_points || ((uintptr_t)out_points & 3)) return TFN_ERR_INVALID_ARGUMENT;
+    const size_t px = (size_t)batch * H * W;
+    if (overlap(out_points, px * 12, input, px * in_bytes(u16)) ||
+        overlap(out_points, px * 12, out_normals, px * 3 * out_bytes(h)))
+        return TFN_ERR_INVALID_ARGUMENT;
+    return run(h, input, u16, disp, batch, H, W, (cudaStream_t)stream, out_normals, out_points, scale);
 }
 
 namespace {

@@ -42,6 +42,15 @@ __global__ void __launch_bounds__(256) tfn_pixel_kernel(KernelArgs p) {
         float* o = reinterpret_cast<float*>(p.out) + i0;
         o[0] = n.x; o[st] = n.y; o[2 * st] = n.z;
     }
+    if (p.pts) {      // N3 point cloud (same formulas as the strip kernel)
+        const float zs = sanitize(sample_f(__ldg(reinterpret_cast<const T*>(p.in) + b * HW + pix)));
+        const float Z = DISP ? __fdiv_rn(p.pscale, zs) : __fmul_rn(zs, p.pscale);
+        const float a = __fsub_rn(__int2float_rn(u), p.u0), bb = __fsub_rn(__int2float_rn(v), p.v0);
+        float* q = p.pts + i0;
+        q[0] = __fmul_rn(__fmul_rn(a, Z), p.ifx);
+        q[st] = __fmul_rn(__fmul_rn(bb, Z), p.ify);
+        q[2 * st] = Z;
+    }
 }
 
 // ------------------------------------------------------------------------------------

@@ -30,6 +30,9 @@ struct KernelArgs {
     int strip_h;         // rows per warp strip (strip kernel)
     int* work;           // zeroed work counter for dynamic strip scheduling (nullptr: static)
     int* fired;          // fast strip variant: += its special row steps (nullptr: not counted)
+    float* pts;          // N3: fp32 point cloud, same layout as the normals (nullptr: none)
+    float pscale;        //   Z = pscale * sample (depth, incl. uint16 codes) or pscale / d (disparity)
+    float ifx, ify;      //   1/fx, 1/fy
 };
 
 cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, int kernel,

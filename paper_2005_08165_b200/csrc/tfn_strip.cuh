@@ -43,6 +43,8 @@ struct StripCtx {
     float a[4];        // u - u0 of the 4 columns
     int* fired;        // AUTO probe: += 1 per row step that needed the special path
     bool f16;          // normals stored as IEEE half (N1), else fp32
+    float* pts;        // N3: this lane's point-cloud output (column cm) of the item's frame, or nullptr
+    float pscale, ifx, ify;   // Z = pscale * sample (depth) or pscale / d (disparity); 1/fx, 1/fy
     float v0;
 };
 
@@ -118,7 +120,7 @@ __device__ __forceinline__ void st4h(void* p, float a, float b, float c, float d
 // One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw holds row v+2 in
 // flight), C = slot(v) (C.raw receives row v+3), N = slot(v+1) (N.raw loaded; the rest
 // computed here).
-template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T>
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
                                          char* __restrict__ out, long long HW, int layout,
                                          unsigned colmask, float vf) {
@@ -280,9 +282,10 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
             }
         }
     }
-    // ---- store (16-B / 8-B aligned: W % 4 == 0, c0 % 4 == 0) ----
+    // ---- store (16-B / 8-B aligned: W % 4 == 0, c0 % 4 == 0).  Half normals and the point
+    //      cloud are general-variant features (the fast variant stays free of their code) ----
     if (c.okm) {
-        if (!c.f16) {
+        if (!GEN || !c.f16) {
             float* o = reinterpret_cast<float*>(out) + v * c.W * (LAYOUT == 0 ? 1 : 3);
             if (LAYOUT == 0) {
                 st4(o, nx[0], nx[1], nx[2], nx[3]);
@@ -305,11 +308,32 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
                 st4h(o + 8, nz[2], nx[3], ny[3], nz[3]);
             }
         }
+        // ---- N3: the point cloud beside the normals, Eq. 13: p = Z (a/fx, b/fy, 1) ----
+        if (PTS) {
+            float X[4], Y[4], Z[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float zs = C.z[i + 1];             // NaN for an invalid sample
+                Z[i] = DISP ? __fdiv_rn(c.pscale, zs) : __fmul_rn(zs, c.pscale);
+                X[i] = __fmul_rn(__fmul_rn(c.a[i], Z[i]), c.ifx);
+                Y[i] = __fmul_rn(__fmul_rn(b, Z[i]), c.ify);
+            }
+            float* q = c.pts + v * c.W * (LAYOUT == 0 ? 1 : 3);
+            if (LAYOUT == 0) {
+                st4(q, X[0], X[1], X[2], X[3]);
+                st4(q + HW, Y[0], Y[1], Y[2], Y[3]);
+                st4(q + 2 * HW, Z[0], Z[1], Z[2], Z[3]);
+            } else {
+                st4(q, X[0], Y[0], Z[0], X[1]);
+                st4(q + 4, Y[1], Z[1], X[2], Y[2]);
+                st4(q + 8, Z[2], X[3], Y[3], Z[3]);
+            }
+        }
     }
 }
 
 // Rows [ys, y1) of one strip: prologue, then the rolling window down the strip.
-template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T>
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS>
 __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long long HW, int layout,
                                           unsigned colmask, int ys, int y1) {
     Slot S0, S1, S2;
@@ -331,11 +355,11 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
     }
     float vf = __int2float_rn(ys);      // exact row index as float (rows < 2^24)
     for (int v = ys; v < y1; v += 3) {
-        row_step<F, MODE, DISP, LAYOUT, GEN, T>(S0, S1, S2, v, c, out, HW, layout, colmask, vf);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS>(S0, S1, S2, v, c, out, HW, layout, colmask, vf);
         if (v + 1 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN, T>(S1, S2, S0, v + 1, c, out, HW, layout, colmask, vf + 1.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS>(S1, S2, S0, v + 1, c, out, HW, layout, colmask, vf + 1.0f);
         if (v + 2 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN, T>(S2, S0, S1, v + 2, c, out, HW, layout, colmask, vf + 2.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS>(S2, S0, S1, v + 2, c, out, HW, layout, colmask, vf + 2.0f);
         vf += 3.0f;
     }
 }
@@ -345,7 +369,7 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
 // per pixel, but no divergent exact-path calls — the better choice when many row steps
 // contain special pixels: holes, salt dropout, integer-quantized depth).  The fast variant
 // counts its special row steps into p.fired (host-side AUTO selection, tfn_abi.cu).
-template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T>
+template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS>
 #ifdef TFN_STRIP_MAXNREG
 __global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(KernelArgs p) {
 #else
@@ -365,6 +389,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
     c.u0 = p.u0; c.v0 = p.v0;
     c.fired = p.fired;
     c.f16 = p.out_f16 != 0;
+    c.pscale = p.pscale; c.ifx = p.ifx; c.ify = p.ify;
     const int es = c.f16 ? 2 : 4;          // bytes per output component
 
     // first item static, the rest claimed from a work counter (load balance: strips with
@@ -392,8 +417,9 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
             if (c0 + 3 == p.W - 1) colmask |= 8u;
         }
         char* out = reinterpret_cast<char*>(p.out) + es * (fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm));
+        c.pts = p.pts ? p.pts + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm) : nullptr;
 
-        strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T>(c, out, HW, p.layout, colmask, y0, y1);
+        strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS>(c, out, HW, p.layout, colmask, y0, y1);
         if (p.work) {
             int nxt = 0;
             if (lane == 0) nxt = atomicAdd(p.work, 1);

@@ -33,8 +33,9 @@ ABI_SYMBOLS = (
     "tfn_create", "tfn_set_layout", "tfn_set_option", "tfn_estimate", "tfn_estimate_disparity",
     "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8", "tfn_destroy", "tfn_status_string",
     "tfn_kernel_launches", "tfn_version", "tfn_debug_sol", "tfn_auto_variant", "tfn_estimate_u16",
-    "tfn_estimate_host_u16",
+    "tfn_estimate_host_u16", "tfn_estimate_points",
 )
+INPUT_KINDS = {"depth": 0, "disparity": 1, "depth_u16": 2}
 
 
 class TfnError(RuntimeError):
@@ -68,6 +69,7 @@ def lib() -> ctypes.CDLL:
         L.tfn_estimate_host.argtypes = [vp, vp, i, d, i, i, i, vp, vp]
         L.tfn_estimate_u16.argtypes = [vp, vp, d, i, i, i, vp, vp]
         L.tfn_estimate_host_u16.argtypes = [vp, vp, d, i, i, i, vp, vp]
+        L.tfn_estimate_points.argtypes = [vp, vp, i, d, i, i, i, vp, vp, vp]
         L.tfn_stats.argtypes = [vp, vp, i, i, i, i, vp, vp]
         L.tfn_debug_phi8.argtypes = [vp, ll, i, vp, vp, vp]
         L.tfn_debug_sol.argtypes = [vp, i, i, i, vp, vp]
@@ -83,7 +85,7 @@ def lib() -> ctypes.CDLL:
                                                      "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8",
                                                      "tfn_destroy", "tfn_version", "tfn_debug_sol",
                                                      "tfn_auto_variant", "tfn_estimate_u16",
-                                                     "tfn_estimate_host_u16"):
+                                                     "tfn_estimate_host_u16", "tfn_estimate_points"):
                 f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -130,6 +132,12 @@ def tfn_estimate_u16(h: int, codes_ptr: int, depth_scale: float, batch: int, H: 
 def tfn_estimate_host_u16(h: int, host_codes: int, depth_scale: float, batch: int, H: int, W: int,
                           host_out: int, stream: int) -> int:
     return lib().tfn_estimate_host_u16(h, host_codes, float(depth_scale), batch, H, W, host_out, stream)
+
+
+def tfn_estimate_points(h: int, in_ptr: int, input_kind: int, scale: float, batch: int, H: int, W: int,
+                        stream: int, out_ptr: int, pts_ptr: int) -> int:
+    return lib().tfn_estimate_points(h, in_ptr, int(input_kind), float(scale), batch, H, W, stream, out_ptr,
+                                     pts_ptr)
 
 
 def tfn_estimate_disparity(h: int, disp_ptr: int, baseline_times_f: float, batch: int, H: int, W: int,
@@ -255,6 +263,30 @@ class Estimator:
         _check(tfn_estimate_disparity(self.h, disp.data_ptr(), baseline_times_f, B, H, W,
                                       _stream_ptr(stream), out.data_ptr()), "tfn_estimate_disparity")
         return out
+
+    def estimate_points(self, x: torch.Tensor, scale: float = 1.0, disparity: bool = False,
+                        out: Optional[torch.Tensor] = None, points: Optional[torch.Tensor] = None,
+                        stream: Optional[torch.cuda.Stream] = None) -> Tuple[torch.Tensor, torch.Tensor]:
+        """N3: normals and the fp32 point cloud (same layout) in one pass.  x: fp32 depth
+        (Z = scale * x), fp32 disparity (disparity=True, Z = scale / d, scale = f * t_c) or
+        uint16 depth codes (Z = scale * code)."""
+        B, H, W = _bhw(x)
+        if x.dtype == torch.uint16:
+            _need(x, "depth", dtype=torch.uint16)
+            kind = INPUT_KINDS["depth_u16"]
+        else:
+            _need(x, "depth")
+            kind = INPUT_KINDS["disparity" if disparity else "depth"]
+        out = self._out(B, H, W, x, out)
+        if points is None:
+            shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
+            points = torch.empty(shape, dtype=torch.float32, device=x.device)
+        _need(points, "points")
+        if points.numel() != 3 * B * H * W:
+            raise TfnError(TFN_ERR_INVALID_ARGUMENT, "points has the wrong size")
+        _check(tfn_estimate_points(self.h, x.data_ptr(), kind, scale, B, H, W, _stream_ptr(stream),
+                                   out.data_ptr(), points.data_ptr()), "tfn_estimate_points")
+        return out, points
 
     def estimate_host(self, host_in: torch.Tensor, is_disparity: bool = False, baseline_times_f: float = 1.0,
                       out: Optional[torch.Tensor] = None,
