@@ -9,7 +9,10 @@ SMI=$!
 python bench.py > gpurun_out/bench_default_${TAG}.log 2>&1; echo "bench_rc=$?" >> gpurun_out/bench_default_${TAG}.log
 kill $SMI
 python bench.py --impl reference > gpurun_out/bench_ref_${TAG}.log 2>&1; echo "ref_rc=$?" >> gpurun_out/bench_ref_${TAG}.log
-for cfg in 1 3 4; do python bench.py --config $cfg --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_cfg${cfg}_${TAG}.log 2>&1; done
+for cfg in 1 3 4 6 7; do python bench.py --config $cfg --steps 20 --warmup 3 --no-cpu > gpurun_out/bench_cfg${cfg}_${TAG}.log 2>&1; done
+python bench.py --config 4 --kernel strip --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_cfg4_fast_${TAG}.log 2>&1
+python bench.py --kernel general --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_cfg2_general_${TAG}.log 2>&1
+python bench.py --out f16 --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_cfg2_f16_${TAG}.log 2>&1
 python bench.py --config 3 --mode mean --filter fd --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_cfg3_fdmean_${TAG}.log 2>&1
 python bench.py --mode mean --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_cfg2_mean_${TAG}.log 2>&1
 python bench.py --layout packed --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_cfg2_packed_${TAG}.log 2>&1
