@@ -139,7 +139,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
     if (kernel == tfn::TFN_KERNEL_AUTO) {
         if (!strip_ok) {
             kernel = tfn::TFN_KERNEL_PIXEL;
-        } else if (in_u16 || h->out_f16 || pts) {
+        } else if (in_u16 || pts) {
             kernel = tfn::TFN_KERNEL_STRIP_GENERAL;     // the only strip variant built for these
         } else {
             std::lock_guard<std::mutex> lk(h->auto_mu);
@@ -157,9 +157,9 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
                     (h->auto_general || (n % TFN_AUTO_PROBE_FAST) == 0);
         }
     }
-    // the fast strip variant is built for fp32 in / fp32 normals only; the general one has the
+    // the fast strip variant is built for fp32 input without points; the general one has the
     // same results (bit for bit) and runs everything else
-    if ((in_u16 || h->out_f16 || pts) && kernel == tfn::TFN_KERNEL_STRIP) kernel = tfn::TFN_KERNEL_STRIP_GENERAL;
+    if ((in_u16 || pts) && kernel == tfn::TFN_KERNEL_STRIP) kernel = tfn::TFN_KERNEL_STRIP_GENERAL;
     const bool strip = (kernel == tfn::TFN_KERNEL_STRIP || kernel == tfn::TFN_KERNEL_STRIP_GENERAL);
     if (strip && !strip_ok) return TFN_ERR_INVALID_ARGUMENT;
     const int gen = (kernel == tfn::TFN_KERNEL_STRIP_GENERAL) ? 1 : 0;

@@ -120,7 +120,7 @@ __device__ __forceinline__ void st4h(void* p, float a, float b, float c, float d
 // One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw holds row v+2 in
 // flight), C = slot(v) (C.raw receives row v+3), N = slot(v+1) (N.raw loaded; the rest
 // computed here).
-template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS>
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
                                          char* __restrict__ out, long long HW, int layout,
                                          unsigned colmask, float vf) {
@@ -282,10 +282,11 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
             }
         }
     }
-    // ---- store (16-B / 8-B aligned: W % 4 == 0, c0 % 4 == 0).  Half normals and the point
-    //      cloud are general-variant features (the fast variant stays free of their code) ----
+    // ---- store (16-B / 8-B aligned: W % 4 == 0, c0 % 4 == 0).  OUT: 0 fp32, 1 half, 2 the
+    //      handle's choice at run time (general variant); the point cloud is general-only ----
     if (c.okm) {
-        if (!GEN || !c.f16) {
+        const bool f16 = (OUT == 2) ? c.f16 : (OUT == 1);
+        if (!f16) {
             float* o = reinterpret_cast<float*>(out) + v * c.W * (LAYOUT == 0 ? 1 : 3);
             if (LAYOUT == 0) {
                 st4(o, nx[0], nx[1], nx[2], nx[3]);
@@ -333,7 +334,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
 }
 
 // Rows [ys, y1) of one strip: prologue, then the rolling window down the strip.
-template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS>
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT>
 __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long long HW, int layout,
                                           unsigned colmask, int ys, int y1) {
     Slot S0, S1, S2;
@@ -355,11 +356,11 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
     }
     float vf = __int2float_rn(ys);      // exact row index as float (rows < 2^24)
     for (int v = ys; v < y1; v += 3) {
-        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS>(S0, S1, S2, v, c, out, HW, layout, colmask, vf);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S0, S1, S2, v, c, out, HW, layout, colmask, vf);
         if (v + 1 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS>(S1, S2, S0, v + 1, c, out, HW, layout, colmask, vf + 1.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S1, S2, S0, v + 1, c, out, HW, layout, colmask, vf + 1.0f);
         if (v + 2 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS>(S2, S0, S1, v + 2, c, out, HW, layout, colmask, vf + 2.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S2, S0, S1, v + 2, c, out, HW, layout, colmask, vf + 2.0f);
         vf += 3.0f;
     }
 }
@@ -369,7 +370,7 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
 // per pixel, but no divergent exact-path calls — the better choice when many row steps
 // contain special pixels: holes, salt dropout, integer-quantized depth).  The fast variant
 // counts its special row steps into p.fired (host-side AUTO selection, tfn_abi.cu).
-template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS>
+template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS, int OUT>
 #ifdef TFN_STRIP_MAXNREG
 __global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(KernelArgs p) {
 #else
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
     c.fx = p.fx; c.fy = p.fy;
     c.u0 = p.u0; c.v0 = p.v0;
     c.fired = p.fired;
-    c.f16 = p.out_f16 != 0;
+    c.f16 = (OUT == 2) ? p.out_f16 != 0 : OUT == 1;
     c.pscale = p.pscale; c.ifx = p.ifx; c.ify = p.ify;
     const int es = c.f16 ? 2 : 4;          // bytes per output component
 
@@ -419,7 +420,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
         char* out = reinterpret_cast<char*>(p.out) + es * (fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm));
         c.pts = p.pts ? p.pts + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm) : nullptr;
 
-        strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS>(c, out, HW, p.layout, colmask, y0, y1);
+        strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS, OUT>(c, out, HW, p.layout, colmask, y0, y1);
         if (p.work) {
             int nxt = 0;
             if (lane == 0) nxt = atomicAdd(p.work, 1);

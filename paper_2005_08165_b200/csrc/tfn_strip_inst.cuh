@@ -4,8 +4,9 @@
 // {planar, packed} x {fast, general}; uint16 depth codes (N1) x {mean, median} x
 // {planar, packed} x {general} (integer-quantized depth makes dZ = 0 common, so the
 // fast variant's special path would run on most row steps); and the general variant with
-// the fused point cloud (N3) for every input.  The fast variant writes fp32 normals only:
-// half normals and points run the general variant (same bits).
+// the fused point cloud (N3) for every input.  The fast variant is compiled per normal
+// dtype (fp32 / half); the general one reads the dtype at run time; points run the general
+// variant (same bits).
 #pragma once
 #include "tfn_device.cuh"
 #include "tfn_kernels.h"
@@ -13,14 +14,20 @@
 
 namespace tfn {
 
-template <int F, int MODE, bool DISP, int KV, class T, bool PTS = false>
+template <int F, int MODE, bool DISP, int KV, class T, bool PTS = false, int OUT = 2>
 static cudaError_t launch_l(const KernelArgs& a, int grid, cudaStream_t st) {
-    if (a.layout == 0) tfn_strip_kernel<F, MODE, DISP, 0, KV, T, PTS><<<grid, TFN_STRIP_THREADS, 0, st>>>(a);
-    else tfn_strip_kernel<F, MODE, DISP, 1, KV, T, PTS><<<grid, TFN_STRIP_THREADS, 0, st>>>(a);
+    if (a.layout == 0) tfn_strip_kernel<F, MODE, DISP, 0, KV, T, PTS, OUT><<<grid, TFN_STRIP_THREADS, 0, st>>>(a);
+    else tfn_strip_kernel<F, MODE, DISP, 1, KV, T, PTS, OUT><<<grid, TFN_STRIP_THREADS, 0, st>>>(a);
     return cudaGetLastError();
 }
 
-// variant 0 = fast (fp32 normals only), 1 = general; half normals / points force general
+template <int F, int MODE, bool DISP>
+static cudaError_t launch_fast(const KernelArgs& a, int grid, cudaStream_t st) {
+    return a.out_f16 ? launch_l<F, MODE, DISP, 0, float, false, 1>(a, grid, st)
+                     : launch_l<F, MODE, DISP, 0, float, false, 0>(a, grid, st);
+}
+
+// variant 0 = fast, 1 = general; uint16 input and points always run general
 template <int F, int MODE>
 static cudaError_t launch_m(const KernelArgs& a, bool disp, int variant, int grid, cudaStream_t st) {
     if (a.in_u16) {
@@ -31,9 +38,8 @@ static cudaError_t launch_m(const KernelArgs& a, bool disp, int variant, int gri
     if (a.pts)
         return disp ? launch_l<F, MODE, true, 1, float, true>(a, grid, st)
                     : launch_l<F, MODE, false, 1, float, true>(a, grid, st);
-    if (a.out_f16) variant = 1;
-    if (disp) return variant ? launch_l<F, MODE, true, 1, float>(a, grid, st) : launch_l<F, MODE, true, 0, float>(a, grid, st);
-    return variant ? launch_l<F, MODE, false, 1, float>(a, grid, st) : launch_l<F, MODE, false, 0, float>(a, grid, st);
+    if (disp) return variant ? launch_l<F, MODE, true, 1, float>(a, grid, st) : launch_fast<F, MODE, true>(a, grid, st);
+    return variant ? launch_l<F, MODE, false, 1, float>(a, grid, st) : launch_fast<F, MODE, false>(a, grid, st);
 }
 
 template <int F>
@@ -53,9 +59,9 @@ static int occ(K kernel) {
 
 template <int F, int MODE>
 static int occ_m(bool disp, int variant, int in_u16) {
-    if (in_u16) return occ(tfn_strip_kernel<F, MODE, false, 0, 1, unsigned short, false>);
-    if (disp) return variant ? occ(tfn_strip_kernel<F, MODE, true, 0, 1, float, false>) : occ(tfn_strip_kernel<F, MODE, true, 0, 0, float, false>);
-    return variant ? occ(tfn_strip_kernel<F, MODE, false, 0, 1, float, false>) : occ(tfn_strip_kernel<F, MODE, false, 0, 0, float, false>);
+    if (in_u16) return occ(tfn_strip_kernel<F, MODE, false, 0, 1, unsigned short, false, 2>);
+    if (disp) return variant ? occ(tfn_strip_kernel<F, MODE, true, 0, 1, float, false, 2>) : occ(tfn_strip_kernel<F, MODE, true, 0, 0, float, false, 0>);
+    return variant ? occ(tfn_strip_kernel<F, MODE, false, 0, 1, float, false, 2>) : occ(tfn_strip_kernel<F, MODE, false, 0, 0, float, false, 0>);
 }
 
 template <int F>
