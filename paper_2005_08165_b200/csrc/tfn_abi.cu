@@ -130,7 +130,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
     a.layout = h->layout;
     // strip kernel: 4-sample vectors in and 4-component vectors out (16 B fp32, 8 B for
     // uint16 / half), and (frame, strip-row, strip-col) items indexed in 32 bits
-    const long long max_items = (long long)((W + 127) / 128) * ((H + 3) / 4) * (long long)batch;
+    const long long max_items = (long long)((W + TFN_STRIP_COLS - 1) / TFN_STRIP_COLS) * ((H + 3) / 4) * (long long)batch;
     const uintptr_t in_al = 4 * in_bytes(in_u16) - 1, out_al = 4 * out_bytes(h) - 1;
     const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & in_al) == 0) && (((uintptr_t)out & out_al) == 0) &&
                           (((uintptr_t)pts & 15) == 0) && max_items < (1LL << 31);
@@ -168,7 +168,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
         const int ctas_sm = in_u16 ? h->strip_ctas_u16 : h->strip_ctas_per_sm[gen][disp];
         const long long resident_warps = (long long)h->sms * ctas_sm * (TFN_STRIP_THREADS / 32);
         int sh = h->strip_h;
-        const long long sx_n = (W + 127) / 128;
+        const long long sx_n = (W + TFN_STRIP_COLS - 1) / TFN_STRIP_COLS;
         if (sh <= 0) {
             // 48 rows per strip (a multiple of the 3-row unroll; measured best on config 2 with
             // dynamic scheduling: 12 -> 192.7, 24 -> 201.1, 48 -> 203.3 Gpx/s); halved while
@@ -201,7 +201,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
         if (!h->fb_pending &&
             cudaMemcpyAsync(h->fb_host, a.fired, sizeof(int), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
             cudaEventRecord(h->fb_ev, st) == cudaSuccess) {
-            h->fb_steps = (double)((W + 127) / 128) * H * (double)batch;
+            h->fb_steps = (double)((W + TFN_STRIP_COLS - 1) / TFN_STRIP_COLS) * H * (double)batch;
             h->fb_pending = true;
         }
         cudaGetLastError();

@@ -10,6 +10,10 @@
 #ifndef TFN_STRIP_MINBLOCKS
 #define TFN_STRIP_MINBLOCKS 3
 #endif
+#ifndef TFN_STRIP_PPL
+#define TFN_STRIP_PPL 4          // strip kernel: pixels (columns) per lane
+#endif
+#define TFN_STRIP_COLS (32 * TFN_STRIP_PPL)   // columns per warp strip
 
 namespace tfn {
 
