@@ -58,7 +58,10 @@ typedef enum {
     TFN_ERR_CUDA = 3              /* CUDA launch/runtime error, or the device is not sm_100 */
 } tfn_status;
 
-typedef enum { TFN_FILTER_FD = 0, TFN_FILTER_SOBEL = 1, TFN_FILTER_SCHARR = 2, TFN_FILTER_PREWITT = 3 } tfn_filter;
+typedef enum {
+    TFN_FILTER_FD = 0, TFN_FILTER_SOBEL = 1, TFN_FILTER_SCHARR = 2, TFN_FILTER_PREWITT = 3,
+    TFN_FILTER_CUSTOM = 4   /* [kp k0 kp]^T (x) [-1 0 1] with run-time weights (tfn_set_filter_weights) */
+} tfn_filter;
 typedef enum { TFN_NZ_MEAN = 0, TFN_NZ_MEDIAN = 1 } tfn_nz_mode;
 typedef enum { TFN_LAYOUT_PLANAR = 0, TFN_LAYOUT_PACKED = 1 } tfn_layout;
 typedef enum { TFN_OUT_F32 = 0, TFN_OUT_F16 = 1 } tfn_out_dtype;
@@ -84,6 +87,15 @@ typedef struct tfn_ctx* tfn_handle;
  * Errors: K or out NULL, bad enum -> INVALID_ARGUMENT; fx/fy/u0/v0 non-finite or
  * fx, fy <= 0 -> CONFIG; no CUDA device / not sm_100 -> CUDA. */
 int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_handle* out);
+
+/* Weights of a TFN_FILTER_CUSTOM handle: the smoothing column [kp k0 kp] of the gradient
+ * kernels [kp k0 kp]^T (x) [-1 0 1] (horizontal; vertical = transpose) — the paper's 3x3
+ * kernel search space.  kp > 0 and k0 > 0, finite (CONFIG
+ * otherwise; kp = 0 is TFN_FILTER_FD).  Only the ratio matters for the direction; the
+ * gradient is summed in the oracle's order ((kp D- + k0 D0) + kp D+), so (1,2), (3,10)
+ * and (1,1) reproduce Sobel, Scharr and Prewitt bit for bit.  Default (1, 2).
+ * INVALID_ARGUMENT if h is NULL or not a CUSTOM handle. */
+int tfn_set_filter_weights(tfn_handle h, double kp, double k0);
 
 /* Output layout (tfn_layout); default PLANAR. */
 int tfn_set_layout(tfn_handle h, int layout);

@@ -36,6 +36,7 @@ struct tfn_ctx {
     int mode;
     int layout = TFN_LAYOUT_PLANAR;
     int out_f16 = 0;                     // TFN_OPT_OUT_DTYPE
+    double kp = 1.0, k0 = 2.0;           // TFN_FILTER_CUSTOM weights (tfn_set_filter_weights)
     int kernel = tfn::TFN_KERNEL_AUTO;
     int strip_h = 0;
     int grid = 0;
@@ -120,6 +121,8 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
     a.pscale = (float)pscale;
     a.ifx = (float)(1.0 / h->K.fx);
     a.ify = (float)(1.0 / h->K.fy);
+    a.kp = h->kp;
+    a.k0 = h->k0;
     a.B = batch;
     a.H = H;
     a.W = W;
@@ -216,7 +219,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
 TFN_API int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_handle* out) {
     if (!K || !out) return TFN_ERR_INVALID_ARGUMENT;
     *out = nullptr;
-    if (filter < 0 || filter > 3 || nz_mode < 0 || nz_mode > 1) return TFN_ERR_INVALID_ARGUMENT;
+    if (filter < 0 || filter > 4 || nz_mode < 0 || nz_mode > 1) return TFN_ERR_INVALID_ARGUMENT;
     if (!is_fin(K->fx) || !is_fin(K->fy) || !is_fin(K->u0) || !is_fin(K->v0) || K->fx <= 0 || K->fy <= 0)
         return TFN_ERR_CONFIG;
     int dev = 0, sms = 0;
@@ -248,6 +251,14 @@ TFN_API int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_han
         h->fb_host = nullptr;             // AUTO then always picks the fast variant
     }
     *out = h;
+    return TFN_OK;
+}
+
+TFN_API int tfn_set_filter_weights(tfn_handle h, double kp, double k0) {
+    if (!h || h->filter != TFN_FILTER_CUSTOM) return TFN_ERR_INVALID_ARGUMENT;
+    if (!is_fin(kp) || !is_fin(k0) || kp <= 0 || k0 <= 0) return TFN_ERR_CONFIG;
+    h->kp = kp;
+    h->k0 = k0;
     return TFN_OK;
 }
 

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) tfn_pixel_kernel(KernelArgs p) {
     if (u >= p.W || v >= p.H) return;
     const long long HW = (long long)p.H * p.W;
     const Normal n = pixel_general<F, MODE, DISP>(reinterpret_cast<const T*>(p.in) + b * HW, p.H, p.W, v, u,
-                                                  p.u0, p.v0, p.fx, p.fy);
+                                                  p.u0, p.v0, p.fx, p.fy, Wts{p.kp, p.k0});
     const long long pix = (long long)v * p.W + u;
     const long long i0 = p.layout == 0 ? b * 3 * HW + pix : (b * HW + pix) * 3;
     const long long st = p.layout == 0 ? HW : 1;
@@ -83,7 +83,8 @@ int strip_occupancy(int filter, int mode, bool disp, int variant, int in_u16) {
     case FD: return occupancy_strip<FD>(mode, disp, variant, in_u16);
     case SOBEL: return occupancy_strip<SOBEL>(mode, disp, variant, in_u16);
     case SCHARR: return occupancy_strip<SCHARR>(mode, disp, variant, in_u16);
-    default: return occupancy_strip<PREWITT>(mode, disp, variant, in_u16);
+    case PREWITT: return occupancy_strip<PREWITT>(mode, disp, variant, in_u16);
+    default: return occupancy_strip<CUSTOM>(mode, disp, variant, in_u16);
     }
 }
 
@@ -93,7 +94,8 @@ cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, in
     case FD: return launch_f<FD>(a, mode, disp, kernel, grid_strip, st);
     case SOBEL: return launch_f<SOBEL>(a, mode, disp, kernel, grid_strip, st);
     case SCHARR: return launch_f<SCHARR>(a, mode, disp, kernel, grid_strip, st);
-    default: return launch_f<PREWITT>(a, mode, disp, kernel, grid_strip, st);
+    case PREWITT: return launch_f<PREWITT>(a, mode, disp, kernel, grid_strip, st);
+    default: return launch_f<CUSTOM>(a, mode, disp, kernel, grid_strip, st);
     }
 }
 

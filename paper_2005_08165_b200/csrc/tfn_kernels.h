@@ -37,6 +37,7 @@ struct KernelArgs {
     float* pts;          // N3: fp32 point cloud, same layout as the normals (nullptr: none)
     float pscale;        //   Z = pscale * sample (depth, incl. uint16 codes) or pscale / d (disparity)
     float ifx, ify;      //   1/fx, 1/fy
+    double kp, k0;       // CUSTOM filter weights [kp k0 kp] (ignored by the fixed filters)
 };
 
 cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, int kernel,

@@ -53,6 +53,7 @@ struct StripCtx {
     bool f16;          // normals stored as IEEE half (N1), else fp32
     float* pts;        // N3: this lane's point-cloud output (column cm) of the item's frame, or nullptr
     float pscale, ifx, ify;   // Z = pscale * sample (depth) or pscale / d (disparity); 1/fx, 1/fy
+    Wts wt;            // CUSTOM filter weights
     float v0;
 };
 
@@ -188,9 +189,9 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     for (int i = 0; i < PPL; ++i) {
         const double dhn = __dsub_rn(N.w[i + 2], N.w[i]);          // D_h(v+1)
         const double dhc = Taps<F>::corners ? __dsub_rn(C.w[i + 2], C.w[i]) : 0.0;   // D_h(v)
-        gu[i] = grad_tail<F>(C.head[i], dhn);
-        N.head[i] = grad_head<F>(dhc, dhn);
-        gv[i] = grad_tail<F>(grad_head<F>(dv[i], dv[i + 1]), dv[i + 2]);
+        gu[i] = grad_tail<F>(C.head[i], dhn, c.wt);
+        N.head[i] = grad_head<F>(dhc, dhn, c.wt);
+        gv[i] = grad_tail<F>(grad_head<F>(dv[i], dv[i + 1], c.wt), dv[i + 2], c.wt);
     }
     float gu32[4], gv32[4], s32[4], t32[4];
 #pragma unroll
@@ -328,7 +329,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         for (int i = 0; i < PPL; ++i) {
             if (special & (1u << i)) {
                 const Normal n = pixel_general<F, MODE, DISP>(c.img, c.H, c.W, v, c.cm + i, c.u0, c.v0,
-                                                              c.fx, c.fy);
+                                                              c.fx, c.fy, c.wt);
                 nx[i] = n.x; ny[i] = n.y; nz[i] = n.z;
             }
         }
@@ -393,7 +394,7 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
 #pragma unroll
     for (int i = 0; i < PPL; ++i) {
         S1.head[i] = grad_head<F>(Taps<F>::corners ? __dsub_rn(S0.w[i + 2], S0.w[i]) : 0.0,
-                                  __dsub_rn(S1.w[i + 2], S1.w[i]));
+                                  __dsub_rn(S1.w[i + 2], S1.w[i]), c.wt);
         const float zc = S1.z[i + 1];
         S1.rN[i] = pair_rcp<DISP>(S0.z[i + 1], zc);
         S1.rNW[i] = pair_rcp<DISP>(S0.z[i], zc);
@@ -434,6 +435,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
     c.fx = p.fx; c.fy = p.fy;
     c.u0 = p.u0; c.v0 = p.v0;
     c.fired = p.fired;
+    c.wt.kp = p.kp; c.wt.k0 = p.k0;
     c.f16 = (OUT == 2) ? p.out_f16 != 0 : OUT == 1;
     c.pscale = p.pscale; c.ifx = p.ifx; c.ify = p.ify;
     const int es = c.f16 ? 2 : 4;          // bytes per output component

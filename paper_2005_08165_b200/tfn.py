@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TFN_LIB") or os.path.join(_HERE, "libtfn.so")
 
 TFN_OK, TFN_ERR_INVALID_ARGUMENT, TFN_ERR_CONFIG, TFN_ERR_CUDA = 0, 1, 2, 3
-FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3}
+FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3, "custom": 4}
 MODES = {"mean": 0, "median": 1}
 LAYOUTS = {"planar": 0, "packed": 1}
 KERNELS = {"auto": 0, "pixel": 1, "strip": 2, "general": 3}
@@ -33,7 +33,7 @@ ABI_SYMBOLS = (
     "tfn_create", "tfn_set_layout", "tfn_set_option", "tfn_estimate", "tfn_estimate_disparity",
     "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8", "tfn_destroy", "tfn_status_string",
     "tfn_kernel_launches", "tfn_version", "tfn_debug_sol", "tfn_auto_variant", "tfn_estimate_u16",
-    "tfn_estimate_host_u16", "tfn_estimate_points",
+    "tfn_estimate_host_u16", "tfn_estimate_points", "tfn_set_filter_weights",
 )
 INPUT_KINDS = {"depth": 0, "disparity": 1, "depth_u16": 2}
 
@@ -70,6 +70,7 @@ def lib() -> ctypes.CDLL:
         L.tfn_estimate_u16.argtypes = [vp, vp, d, i, i, i, vp, vp]
         L.tfn_estimate_host_u16.argtypes = [vp, vp, d, i, i, i, vp, vp]
         L.tfn_estimate_points.argtypes = [vp, vp, i, d, i, i, i, vp, vp, vp]
+        L.tfn_set_filter_weights.argtypes = [vp, d, d]
         L.tfn_stats.argtypes = [vp, vp, i, i, i, i, vp, vp]
         L.tfn_debug_phi8.argtypes = [vp, ll, i, vp, vp, vp]
         L.tfn_debug_sol.argtypes = [vp, i, i, i, vp, vp]
@@ -85,7 +86,8 @@ def lib() -> ctypes.CDLL:
                                                      "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8",
                                                      "tfn_destroy", "tfn_version", "tfn_debug_sol",
                                                      "tfn_auto_variant", "tfn_estimate_u16",
-                                                     "tfn_estimate_host_u16", "tfn_estimate_points"):
+                                                     "tfn_estimate_host_u16", "tfn_estimate_points",
+                                                     "tfn_set_filter_weights"):
                 f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -110,6 +112,10 @@ def tfn_create(K, filter: int, nz_mode: int) -> int:
     h = ctypes.c_void_p()
     _check(lib().tfn_create(ctypes.byref(k), int(filter), int(nz_mode), ctypes.byref(h)), "tfn_create")
     return h.value
+
+
+def tfn_set_filter_weights(h: int, kp: float, k0: float) -> None:
+    _check(lib().tfn_set_filter_weights(h, float(kp), float(k0)), "tfn_set_filter_weights")
 
 
 def tfn_set_layout(h: int, layout: int) -> None:
@@ -220,7 +226,11 @@ class Estimator:
         self.filter, self.nz_mode, self.layout = filter, nz_mode, layout
         self.out_dtype = out_dtype
         self._odt = torch.float16 if out_dtype == "f16" else torch.float32
-        self.h = tfn_create(self.K, FILTERS[filter], MODES[nz_mode])
+        # filter: a name, or the (kp, k0) weights of [kp k0 kp]^T (x) [-1 0 1] (TFN_FILTER_CUSTOM)
+        custom = isinstance(filter, (tuple, list))
+        self.h = tfn_create(self.K, FILTERS["custom" if custom else filter], MODES[nz_mode])
+        if custom:
+            tfn_set_filter_weights(self.h, float(filter[0]), float(filter[1]))
         tfn_set_layout(self.h, LAYOUTS[layout])
         tfn_set_option(self.h, OPT_KERNEL, KERNELS[kernel])
         tfn_set_option(self.h, OPT_STRIP_H, strip_h)

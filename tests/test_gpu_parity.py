@@ -454,3 +454,37 @@ def test_noise_degrades_accuracy_monotonically(tfn, random8):
             acc = tfn.stats(est.estimate(z), gt).cpu().numpy()
             aae.append(acc[0] / 1e6 / acc[1])
         assert all(a < b for a, b in zip(aae, aae[1:])), (m, aae)
+
+
+# ------------------------------------------------------------------ N1: run-time (p, q) weights
+@pytest.mark.parametrize("w", [(1.0, 4.0), (0.5, 3.7), (2.5, 1.0), (1e-3, 1.0)])
+def test_custom_weights_parity(tfn, random8, w):
+    """TFN_FILTER_CUSTOM: the [kp k0 kp] family of the paper's 3x3 kernel search
+    against the oracle with the same weights; fast, general and per-pixel kernels agree bit
+    for bit (holes and quantized depth included)"""
+    z = random8.depth.numpy()[:2].copy()
+    z[:, 100:140, 200:260] = 0.0
+    zq = (np.round(random8.depth64.numpy()[2:3] * 1000.0) / 1000.0).astype(np.float32)
+    for m in MODES:
+        for x in (z, zq):
+            g, _ = check(tfn, x, ts.K_VGA, w, m)
+            for kernel in ("strip", "general", "pixel"):
+                gk = run_gpu(tfn, x, ts.K_VGA, w, m, kernel=kernel)
+                assert np.array_equal(g.view(np.uint32), gk.view(np.uint32)), (w, m, kernel)
+
+
+def test_custom_weights_reproduce_named_kernels(tfn, random8):
+    """(1,2), (3,10), (1,1) are Sobel, Scharr, Prewitt bit for bit (same fp64 sums)"""
+    z = random8.depth.numpy()[:2]
+    for name, w in (("sobel", (1.0, 2.0)), ("scharr", (3.0, 10.0)), ("prewitt", (1.0, 1.0))):
+        for m in MODES:
+            a = run_gpu(tfn, z, ts.K_VGA, name, m)
+            b = run_gpu(tfn, z, ts.K_VGA, w, m)
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (name, m)
+    from paper_2005_08165_b200 import tfn as T
+    est = tfn.Estimator(ts.K_VGA, (1.0, 2.0), "median")
+    for bad in ((0.0, 1.0), (1.0, 0.0), (-1.0, 2.0), (float("nan"), 1.0)):
+        with pytest.raises(T.TfnError):
+            T.tfn_set_filter_weights(est.h, *bad)
+    with pytest.raises(T.TfnError):
+        T.tfn_set_filter_weights(tfn.Estimator(ts.K_VGA, "sobel", "median").h, 1.0, 2.0)

@@ -47,7 +47,7 @@ def test_p1_spec_slanted_plane(golden):
             np.testing.assert_allclose(inner, np.tile(fx["normal"], (inner.shape[0], 1)), atol=1e-12)
 
 
-@pytest.mark.parametrize("f", FILTERS)
+@pytest.mark.parametrize("f", FILTERS + ((0.5, 3.7), (2.5, 1.0)))
 def test_p1_tilted_plane_analytic(f):
     """Eq. 14: on a plane 1/z is affine in (u,v), so every kernel and
     both Phi recover the exact camera-facing normal (fp64 analytic input)."""
