@@ -57,9 +57,11 @@ def sampled(g, frame, K, f, m, rng, n=2000, disp=False, tol=TOL_DEG):
 
 
 def warm(est, call, n=5):
+    """the bench's warm-up calls; synchronised one by one so that AUTO's asynchronous
+    special-rate read-back (a pinned word + event) is visible to the next call"""
     for _ in range(n):
         call()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
 
 
 def test_full_size_config3_disparity(tfn):
