@@ -59,6 +59,9 @@ def lib():
         L.orc_valid_sample.argtypes = [ctypes.c_double]; L.orc_valid_sample.restype = ctypes.c_int
         L.orc_backproject.argtypes = [Kp, ctypes.c_double, ctypes.c_double, ctypes.c_double, dp]
         L.orc_backproject_image.argtypes = [Kp, dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, dp]
+        L.orc_smallest_eigvec_sym.argtypes = [dp, ctypes.c_int, dp]; L.orc_smallest_eigvec_sym.restype = ctypes.c_int
+        L.orc_plane_fit.argtypes = [dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, Kp, ctypes.c_int, dp]
+        L.orc_plane_fit.restype = ctypes.c_int
         L.orc_inverse_depth.argtypes = [ctypes.c_double]; L.orc_inverse_depth.restype = ctypes.c_double
         L.orc_disparity_to_depth.argtypes = [ctypes.c_double, ctypes.c_double]
         L.orc_disparity_to_depth.restype = ctypes.c_double
@@ -134,6 +137,34 @@ def backproject_image(depth: np.ndarray, K) -> np.ndarray:
     out = np.empty((B, 3, H, W), dtype=np.float64)
     k = _kstruct(K)
     lib().orc_backproject_image(ctypes.byref(k), _dp(z), B, H, W, _dp(out))
+    return out
+
+
+def smallest_eigvec_sym(M: np.ndarray) -> np.ndarray:
+    """SPEC S:276-280 (N4 plumbing): unit eigenvector of the smallest eigenvalue (Jacobi)."""
+    m = np.ascontiguousarray(M, dtype=np.float64)
+    d = m.shape[0]
+    out = np.empty(d)
+    if lib().orc_smallest_eigvec_sym(_dp(m), d, _dp(out)) != 0:
+        raise ValueError("matrix is not symmetric")
+    return out
+
+
+PLANE_METHODS = {"pca": 0, "svd": 1}
+
+
+def plane_fit(depth: np.ndarray, K, method: str = "pca") -> np.ndarray:
+    """PlanePCA (Eq. 3) / PlaneSVD (Eq. 2) normals [B,3,H,W] fp64 of depth
+    [B,H,W] (3x3 window, k >= 3 valid neighbours, border invalid, oriented
+    toward the camera)."""
+    z = np.ascontiguousarray(depth, dtype=np.float64)
+    if z.ndim == 2:
+        z = z[None]
+    B, H, W = z.shape
+    out = np.empty((B, 3, H, W), dtype=np.float64)
+    k = _kstruct(K)
+    if lib().orc_plane_fit(_dp(z), B, H, W, ctypes.byref(k), PLANE_METHODS[method], _dp(out)) != 0:
+        raise ValueError(method)
     return out
 
 

@@ -320,3 +320,136 @@ ORC_EXPORT int orc_estimate_pixel_f32(const float* frame, int is_disp, double f_
     for (int c = 0; c < 3; ++c) n_out[c] = border ? NAN : out[c * 25 + 12];
     return 0;
 }
+
+/* ================================================================================
+ * the comparison estimators PlaneSVD (Eq. 2) and
+ * PlanePCA (Eq. 3), as SPEC S:251-258 specifies them: per pixel, the centre
+ * point and its valid 8-neighbours Q_i^+ (k >= 3 neighbours, else invalid; 1-px border
+ * invalid), back-projected with Eq. 13; PlaneSVD = the smallest-eigenvalue eigenvector of
+ * the 4x4 normal matrix [Q+ 1]^T [Q+ 1], n = its first three components; PlanePCA = the
+ * smallest-eigenvalue eigenvector of the 3x3 scatter matrix of Q+ about its mean; then
+ * normalised and oriented toward the camera (Q11).
+ * ================================================================================ */
+
+/* cyclic Jacobi on a symmetric d x d matrix (d = 3 or 4), sweeps until the
+ * off-diagonal Frobenius norm is below 1e-12 x the matrix's Frobenius norm (reading: the
+ * SPEC's 1e-12 taken relative, so the test does not depend on the depth unit), at most 50
+ * sweeps; returns the unit eigenvector of the smallest eigenvalue, ties broken toward the
+ * candidate whose first nonzero component has the largest magnitude (lowest index among
+ * equals), made positive.  Returns 1 if M is not symmetric within 1e-9 (relative). */
+ORC_EXPORT int orc_smallest_eigvec_sym(const double* M, int d, double* out)
+{
+    double a[16], v[16];
+    double fro = 0.0;
+    for (int i = 0; i < d * d; ++i) fro += M[i] * M[i];
+    fro = sqrt(fro);
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j)
+            if (fabs(M[i * d + j] - M[j * d + i]) > 1e-9 * (fro > 0 ? fro : 1.0)) return 1;
+    for (int i = 0; i < d * d; ++i) { a[i] = M[i]; v[i] = (i / d == i % d) ? 1.0 : 0.0; }
+    for (int sweep = 0; sweep < 50; ++sweep) {
+        double off = 0.0;
+        for (int i = 0; i < d; ++i)
+            for (int j = 0; j < d; ++j)
+                if (i != j) off += a[i * d + j] * a[i * d + j];
+        if (sqrt(off) <= 1e-12 * fro) break;
+        for (int p = 0; p < d - 1; ++p)
+            for (int q = p + 1; q < d; ++q) {
+                const double apq = a[p * d + q];
+                if (apq == 0.0) continue;
+                /* Golub & Van Loan, symmetric Schur: zero a_pq */
+                const double theta = (a[q * d + q] - a[p * d + p]) / (2.0 * apq);
+                const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+                const double c = 1.0 / sqrt(1.0 + t * t), s = t * c;
+                for (int k = 0; k < d; ++k) {          /* A <- J^T A J */
+                    const double akp = a[k * d + p], akq = a[k * d + q];
+                    a[k * d + p] = c * akp - s * akq;
+                    a[k * d + q] = s * akp + c * akq;
+                }
+                for (int k = 0; k < d; ++k) {
+                    const double apk = a[p * d + k], aqk = a[q * d + k];
+                    a[p * d + k] = c * apk - s * aqk;
+                    a[q * d + k] = s * apk + c * aqk;
+                }
+                for (int k = 0; k < d; ++k) {          /* V <- V J */
+                    const double vkp = v[k * d + p], vkq = v[k * d + q];
+                    v[k * d + p] = c * vkp - s * vkq;
+                    v[k * d + q] = s * vkp + c * vkq;
+                }
+            }
+    }
+    double lmin = a[0];
+    for (int i = 1; i < d; ++i) if (a[i * d + i] < lmin) lmin = a[i * d + i];
+    const double tie = 1e-12 * (fro > 0 ? fro : 1.0);
+    int best = -1;
+    double best_mag = -1.0;
+    for (int j = 0; j < d; ++j) {
+        if (a[j * d + j] - lmin > tie) continue;
+        double first = 0.0;
+        for (int k = 0; k < d; ++k) if (v[k * d + j] != 0.0) { first = v[k * d + j]; break; }
+        if (fabs(first) > best_mag) { best_mag = fabs(first); best = j; }
+    }
+    double first = 0.0;
+    for (int k = 0; k < d; ++k) if (v[k * d + best] != 0.0) { first = v[k * d + best]; break; }
+    const double sg = first < 0 ? -1.0 : 1.0;
+    for (int k = 0; k < d; ++k) out[k] = sg * v[k * d + best];
+    return 0;
+}
+
+/* method 0 = PlanePCA (Eq. 3), 1 = PlaneSVD (Eq. 2).  depth fp64 [B,H,W]; out planar
+ * [B,3,H,W] fp64, NaN triple where invalid. */
+ORC_EXPORT int orc_plane_fit(const double* depth, int B, int H, int W, const orc_intrinsics* K, int method,
+                             double* out)
+{
+    if (method != 0 && method != 1) return 1;
+    const size_t hw = (size_t)H * W;
+    for (int b = 0; b < B; ++b) {
+        const double* z = depth + (size_t)b * hw;
+        for (int v = 0; v < H; ++v)
+            for (int u = 0; u < W; ++u) {
+                double* o = out + (size_t)b * 3 * hw + (size_t)v * W + u;
+                o[0] = o[hw] = o[2 * hw] = NAN;
+                if (u < 1 || v < 1 || u > W - 2 || v > H - 2) continue;      /* border */
+                const double zc = z[(size_t)v * W + u];
+                if (!orc_valid_sample(zc)) continue;
+                double q[9][3];
+                int n = 0, k = 0;
+                for (int dv = -1; dv <= 1; ++dv)
+                    for (int du = -1; du <= 1; ++du) {
+                        const double zz = z[(size_t)(v + dv) * W + (u + du)];
+                        if (!orc_valid_sample(zz)) continue;
+                        orc_backproject(K, (double)(u + du), (double)(v + dv), zz, q[n]);
+                        ++n;
+                        if (du != 0 || dv != 0) ++k;
+                    }
+                if (k < 3) continue;
+                double nrm[4], M[16];
+                if (method == 0) {
+                    double mean[3] = {0, 0, 0};
+                    for (int i = 0; i < n; ++i) for (int c = 0; c < 3; ++c) mean[c] += q[i][c];
+                    for (int c = 0; c < 3; ++c) mean[c] /= n;
+                    for (int r = 0; r < 3; ++r)
+                        for (int c = 0; c < 3; ++c) {
+                            double s = 0.0;
+                            for (int i = 0; i < n; ++i) s += (q[i][r] - mean[r]) * (q[i][c] - mean[c]);
+                            M[r * 3 + c] = s;
+                        }
+                    if (orc_smallest_eigvec_sym(M, 3, nrm)) continue;
+                } else {
+                    for (int r = 0; r < 4; ++r)
+                        for (int c = 0; c < 4; ++c) {
+                            double s = 0.0;
+                            for (int i = 0; i < n; ++i) s += (r < 3 ? q[i][r] : 1.0) * (c < 3 ? q[i][c] : 1.0);
+                            M[r * 4 + c] = s;
+                        }
+                    if (orc_smallest_eigvec_sym(M, 4, nrm)) continue;
+                }
+                double nn[3] = {nrm[0], nrm[1], nrm[2]};
+                double p[3];
+                orc_backproject(K, (double)u, (double)v, zc, p);
+                orc_orient_toward_camera(nn, p);
+                o[0] = nn[0]; o[hw] = nn[1]; o[2 * hw] = nn[2];
+            }
+    }
+    return 0;
+}
