@@ -151,6 +151,17 @@ int tfn_estimate_points(tfn_handle h, const void* input, int input_kind, double 
 int tfn_estimate_host_u16(tfn_handle h, const unsigned short* host_codes, double depth_scale, int batch, int H,
                           int W, void* host_out, void* stream);
 
+/* the paper's accuracy yardsticks on the GPU: PlanePCA (Eq. 3,
+ * method TFN_PLANE_PCA) or PlaneSVD (Eq. 2, TFN_PLANE_SVD) normals of fp32 depth, per SPEC
+ * the centre and its valid 8-neighbours back-projected (Eq. 13), >= 3 valid
+ * neighbours else invalid, 1-px border invalid, smallest-eigenvalue eigenvector of the 3x3
+ * scatter / 4x4 normal matrix (cyclic Jacobi, fp64), oriented toward the camera.
+ * out_normals: fp32 in the handle's layout (the output dtype option does not apply).
+ * Uses the handle's intrinsics; its filter / Phi are irrelevant.  One thread per pixel. */
+typedef enum { TFN_PLANE_PCA = 0, TFN_PLANE_SVD = 1 } tfn_plane_method;
+int tfn_plane_fit(tfn_handle h, const float* depth, int method, int batch, int H, int W, void* stream,
+                  float* out_normals);
+
 /* angular-error statistics (Eq. 22-24) of est (device,
  * layout `layout`) against gt (device, planar [batch,3,H,W], NaN = invalid), ADDED
  * into stats_dev (device int64[8]): [0] sum of psi in 1e-6 degree units, [1] m =

@@ -12,7 +12,7 @@ from .tfn import (ABI_SYMBOLS, Estimator, TfnError, debug_phi8, debug_sol, lib, 
                   tfn_debug_phi8, tfn_destroy, tfn_estimate, tfn_estimate_disparity, tfn_estimate_host,
                   tfn_kernel_launches, tfn_set_layout, tfn_set_option, tfn_stats, tfn_status_string,
                   tfn_version, tfn_auto_variant, tfn_estimate_u16, tfn_estimate_host_u16, tfn_estimate_points,
-                  tfn_set_filter_weights, STAT_KEYS,
+                  tfn_set_filter_weights, tfn_plane_fit, STAT_KEYS,
                   LIB_PATH)
 
 __all__ = ["Estimator", "TfnError", "stats", "debug_phi8", "lib", "LIB_PATH", "ABI_SYMBOLS", "STAT_KEYS"]

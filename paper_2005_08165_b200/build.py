@@ -13,7 +13,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtfn.so")
 SOURCES = ["tfn_abi.cu", "tfn_kernels.cu", "tfn_stats.cu", "tfn_strip_fd.cu", "tfn_strip_sobel.cu",
-           "tfn_strip_scharr.cu", "tfn_strip_prewitt.cu", "tfn_strip_custom.cu"]
+           "tfn_strip_scharr.cu", "tfn_strip_prewitt.cu", "tfn_strip_custom.cu",
+           "tfn_planefit.cu"]
 HEADERS = ["tfn_device.cuh", "tfn_kernels.h", "tfn_strip.cuh", "tfn_strip_inst.cuh",
            os.path.join("..", "..", "include", "tfn.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -429,6 +429,21 @@ TFN_API int tfn_estimate_host_u16(tfn_handle h, const unsigned short* host_codes
     return host_run(h, host_codes, 1, false, batch, H, W, host_out, stream);
 }
 
+TFN_API int tfn_plane_fit(tfn_handle h, const float* depth, int method, int batch, int H, int W, void* stream,
+                          float* out_normals) {
+    if (!h || (method != TFN_PLANE_PCA && method != TFN_PLANE_SVD)) return TFN_ERR_INVALID_ARGUMENT;
+    if (batch < 0 || H <= 0 || W <= 0) return TFN_ERR_INVALID_ARGUMENT;
+    if (batch == 0) return TFN_OK;
+    if (!depth || !out_normals || ((uintptr_t)depth & 3) || ((uintptr_t)out_normals & 3)) return TFN_ERR_INVALID_ARGUMENT;
+    const size_t px = (size_t)batch * H * W;
+    if (overlap(depth, px * 4, out_normals, px * 12)) return TFN_ERR_INVALID_ARGUMENT;
+    if (tfn::launch_planefit(depth, out_normals, batch, H, W, h->K.fx, h->K.fy, h->K.u0, h->K.v0, h->layout,
+                             method, (cudaStream_t)stream) != cudaSuccess)
+        return TFN_ERR_CUDA;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return TFN_OK;
+}
+
 TFN_API int tfn_stats(const float* est, const float* gt, int batch, int H, int W, int layout, void* stream,
                       long long* stats_dev) {
     if (batch < 0 || H <= 0 || W <= 0 || (layout != 0 && layout != 1)) return TFN_ERR_INVALID_ARGUMENT;

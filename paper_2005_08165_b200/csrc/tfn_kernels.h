@@ -52,6 +52,10 @@ cudaError_t launch_strip(const KernelArgs& a, int mode, bool disp, int variant, 
 template <int F>
 int occupancy_strip(int mode, bool disp, int variant, int in_u16);
 
+// N4: PlanePCA (method 0) / PlaneSVD (method 1) comparator, fp32 normals (tfn_planefit.cu)
+cudaError_t launch_planefit(const float* depth, float* out, long long B, int H, int W, double fx, double fy,
+                            double u0, double v0, int layout, int method, cudaStream_t st);
+
 // a8: angular-error statistics vs ground truth (off the timed path)
 cudaError_t launch_stats(const float* est, const float* gt, long long B, int H, int W,
                          int layout, long long* stats_dev, cudaStream_t st);

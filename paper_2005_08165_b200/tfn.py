@@ -33,8 +33,9 @@ ABI_SYMBOLS = (
     "tfn_create", "tfn_set_layout", "tfn_set_option", "tfn_estimate", "tfn_estimate_disparity",
     "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8", "tfn_destroy", "tfn_status_string",
     "tfn_kernel_launches", "tfn_version", "tfn_debug_sol", "tfn_auto_variant", "tfn_estimate_u16",
-    "tfn_estimate_host_u16", "tfn_estimate_points", "tfn_set_filter_weights",
+    "tfn_estimate_host_u16", "tfn_estimate_points", "tfn_set_filter_weights", "tfn_plane_fit",
 )
+PLANE_METHODS = {"pca": 0, "svd": 1}
 INPUT_KINDS = {"depth": 0, "disparity": 1, "depth_u16": 2}
 
 
@@ -71,6 +72,7 @@ def lib() -> ctypes.CDLL:
         L.tfn_estimate_host_u16.argtypes = [vp, vp, d, i, i, i, vp, vp]
         L.tfn_estimate_points.argtypes = [vp, vp, i, d, i, i, i, vp, vp, vp]
         L.tfn_set_filter_weights.argtypes = [vp, d, d]
+        L.tfn_plane_fit.argtypes = [vp, vp, i, i, i, i, vp, vp]
         L.tfn_stats.argtypes = [vp, vp, i, i, i, i, vp, vp]
         L.tfn_debug_phi8.argtypes = [vp, ll, i, vp, vp, vp]
         L.tfn_debug_sol.argtypes = [vp, i, i, i, vp, vp]
@@ -87,7 +89,7 @@ def lib() -> ctypes.CDLL:
                                                      "tfn_destroy", "tfn_version", "tfn_debug_sol",
                                                      "tfn_auto_variant", "tfn_estimate_u16",
                                                      "tfn_estimate_host_u16", "tfn_estimate_points",
-                                                     "tfn_set_filter_weights"):
+                                                     "tfn_set_filter_weights", "tfn_plane_fit"):
                 f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -112,6 +114,11 @@ def tfn_create(K, filter: int, nz_mode: int) -> int:
     h = ctypes.c_void_p()
     _check(lib().tfn_create(ctypes.byref(k), int(filter), int(nz_mode), ctypes.byref(h)), "tfn_create")
     return h.value
+
+
+def tfn_plane_fit(h: int, depth_ptr: int, method: int, batch: int, H: int, W: int, stream: int,
+                  out_ptr: int) -> int:
+    return lib().tfn_plane_fit(h, depth_ptr, int(method), batch, H, W, stream, out_ptr)
 
 
 def tfn_set_filter_weights(h: int, kp: float, k0: float) -> None:
@@ -297,6 +304,19 @@ class Estimator:
         _check(tfn_estimate_points(self.h, x.data_ptr(), kind, scale, B, H, W, _stream_ptr(stream),
                                    out.data_ptr(), points.data_ptr()), "tfn_estimate_points")
         return out, points
+
+    def plane_fit(self, depth: torch.Tensor, method: str = "pca", out: Optional[torch.Tensor] = None,
+                  stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """N4 comparator: PlanePCA / PlaneSVD normals (fp32, the handle's layout)."""
+        _need(depth, "depth")
+        B, H, W = _bhw(depth)
+        if out is None:
+            shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
+            out = torch.empty(shape, dtype=torch.float32, device=depth.device)
+        _need(out, "out")
+        _check(tfn_plane_fit(self.h, depth.data_ptr(), PLANE_METHODS[method], B, H, W, _stream_ptr(stream),
+                             out.data_ptr()), "tfn_plane_fit")
+        return out
 
     def estimate_host(self, host_in: torch.Tensor, is_disparity: bool = False, baseline_times_f: float = 1.0,
                       out: Optional[torch.Tensor] = None,
