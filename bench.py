@@ -103,14 +103,15 @@ def load_peaks():
         return 6650.0, "fallback"
 
 
-def load_traffic(cfg_id, filt, mode, layout, px_per_launch):
-    """DRAM bytes (read + write, GB) per launch of the same kernel/launch size, from the
-    committed ncu --set full capture (profiles/ncu_traffic.json), else None."""
+def load_traffic(cfg_id, filt, mode, layout, px_per_launch, out_dtype="f32", kernel="auto"):
+    """DRAM bytes (read + write, GB) per launch of the same kernel variant / output dtype /
+    launch size, from the committed ncu --set full captures (profiles/ncu_traffic.json),
+    else None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(f"config{cfg_id}:{filt}:{mode}:{layout}")
+        e = d.get(f"config{cfg_id}:{filt}:{mode}:{layout}:{out_dtype}:{kernel}")
         if e and int(e["launch_px"]) == int(px_per_launch):
             return float(e["GB_per_launch"])
     except Exception:
@@ -462,7 +463,7 @@ def main():
         cpu = cpu_baseline(cfg, filt, mode, args.cpu_seconds, args.seed)
 
     if rank == 0:
-        traffic = load_traffic(args.config, filt, mode, args.layout, px_per_launch)
+        traffic = load_traffic(args.config, filt, mode, args.layout, px_per_launch, out_dtype, args.kernel)
         line = {
             "metric": METRIC, "value": value, "unit": "Mpixel/s", "n_gpus": ws, "steps": steps,
             "warmup": args.warmup, "ms_per_step": total_ms_max / steps, "higher_is_better": True,
