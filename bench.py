@@ -70,7 +70,7 @@ def parse():
     ap.add_argument("--filter", default=None)
     ap.add_argument("--mode", default=None)
     ap.add_argument("--layout", default="planar", choices=["planar", "packed"])
-    ap.add_argument("--out", default=None, choices=["f32", "f16"], help="normal dtype (default: the config's)")
+    ap.add_argument("--out", default=None, choices=["f32", "f16", "oct16"], help="normal encoding (default: the config's)")
     ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
     ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel", "general"])
     ap.add_argument("--strip-h", type=int, default=0)
@@ -324,9 +324,10 @@ def main():
     chunk = min(per_rank, 1024) if streaming_cfg else per_rank
 
     out_dtype = args.out or cfg.get("out", "f32")
-    odt = torch.float16 if out_dtype == "f16" else torch.float32
+    odt = {"f32": torch.float32, "f16": torch.float16, "oct16": torch.int16}[out_dtype]
+    ncomp = 2 if out_dtype == "oct16" else 3
     in_b = 2 if cfg.get("u16") else 4
-    bytes_px = in_b + 3 * (2 if out_dtype == "f16" else 4)
+    bytes_px = in_b + {"f32": 12, "f16": 6, "oct16": 4}[out_dtype]
     est = tfn.Estimator(K, filter=filt, nz_mode=mode, layout=args.layout, kernel=args.kernel,
                         strip_h=args.strip_h, grid=args.grid, dynamic=not args.static, out_dtype=out_dtype)
     stream = torch.cuda.current_stream(dev)
@@ -338,7 +339,7 @@ def main():
             est.estimate(x, out=out, stream=stream, depth_scale=DEPTH_SCALE)
 
     x, gt = make_frames(cfg, chunk, first, args.seed, dev)
-    out = torch.empty((chunk, 3, H, W) if args.layout == "planar" else (chunk, H, W, 3),
+    out = torch.empty((chunk, ncomp, H, W) if args.layout == "planar" else (chunk, H, W, ncomp),
                       dtype=odt, device=dev)
     torch.cuda.synchronize()
     for _ in range(max(args.warmup, 3 if not args.profile else args.warmup)):
@@ -409,7 +410,9 @@ def main():
 
     # a8 accuracy statistics vs analytic GT (off the timed region), NCCL all-reduce of int64
     if not streaming_cfg and not args.profile:
-        tfn.stats(out if odt == torch.float32 else out.float(), gt, layout=args.layout, acc=acc, stream=stream)
+        est_f32 = out if odt == torch.float32 else (out.float() if odt == torch.float16
+                                                     else tfn.decode_oct16(out, args.layout).contiguous())
+        tfn.stats(est_f32, gt, layout=args.layout, acc=acc, stream=stream)
     tdist.allreduce_stats(acc)                 # the only collective (NCCL, int64 SUM)
     st = acc.cpu().tolist()
     accuracy = None
@@ -469,7 +472,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": total_ms_max / steps, "higher_is_better": True,
             "scaling": "weak" if not streaming_cfg else "strong", "vs_baseline": None,
             "dtype": "f32 (fp64 gradient path)" + (", u16 depth codes in" if cfg.get("u16") else "") +
-                     (", f16 normals out" if out_dtype == "f16" else ""),
+                     ({"f16": ", f16 normals out", "oct16": ", oct16 normals out"}.get(out_dtype, "")),
             "data": "synthetic (seeded analytic ray-cast scenes)",
             "config": {"workload": cfg["desc"], "filter": filt, "nz_mode": mode, "layout": args.layout,
                        "input": "disparity" if cfg["disp"] else ("depth u16 mm codes" if cfg.get("u16") else "depth"),

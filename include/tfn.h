@@ -25,6 +25,12 @@
  * TFN_OUT_F16: each component the fp32 result rounded to nearest; NaN stays NaN):
  *   TFN_LAYOUT_PLANAR  [batch, 3, H, W]  (n_x plane, n_y plane, n_z plane)
  *   TFN_LAYOUT_PACKED  [batch, H, W, 3]
+ * or octahedral int16 pairs (TFN_OUT_OCT16, 4 B/pixel; [batch,2,H,W] planar / [batch,H,W,2]
+ * packed): (u, v) = round(32767 * octahedral map of (n_x, n_y, -n_z)) — p = v/|v|_1, the
+ * far hemisphere (n_z > 0) folded as (1-|p_y|, 1-|p_x|) with the signs of p — so
+ * camera-facing normals sit in the inner diamond; decode p = q/32767, v = (p_x, p_y,
+ * 1-|p_x|-|p_y|), unfold if negative, normalise, n = (v_x, v_y, -v_z).  Direction error
+ * <= 0.005 deg.  Invalid pixels: (-32768, -32768).
  * An output pixel is VALID iff it is not on the 1-pixel image border, its centre
  * sample is valid and every tap with a nonzero weight in either gradient kernel is
  * valid (FD: the 4 edge neighbours; Sobel/Scharr/Prewitt: all 8).  Invalid output
@@ -64,7 +70,7 @@ typedef enum {
 } tfn_filter;
 typedef enum { TFN_NZ_MEAN = 0, TFN_NZ_MEDIAN = 1 } tfn_nz_mode;
 typedef enum { TFN_LAYOUT_PLANAR = 0, TFN_LAYOUT_PACKED = 1 } tfn_layout;
-typedef enum { TFN_OUT_F32 = 0, TFN_OUT_F16 = 1 } tfn_out_dtype;
+typedef enum { TFN_OUT_F32 = 0, TFN_OUT_F16 = 1, TFN_OUT_OCT16 = 2 } tfn_out_dtype;
 
 /* Options for tfn_set_option (tuning / testing; defaults are the production path) */
 typedef enum {

@@ -8,11 +8,11 @@ CUDA kernels behind the C ABI include/tfn.h (libtfn.so), with a thin ctypes bind
 
 See DESIGN.md for the method, the boundary and the kernel design.
 """
-from .tfn import (ABI_SYMBOLS, Estimator, TfnError, debug_phi8, debug_sol, lib, stats, tfn_create,  # noqa: F401
+from .tfn import (ABI_SYMBOLS, Estimator, decode_oct16, TfnError, debug_phi8, debug_sol, lib, stats, tfn_create,  # noqa: F401
                   tfn_debug_phi8, tfn_destroy, tfn_estimate, tfn_estimate_disparity, tfn_estimate_host,
                   tfn_kernel_launches, tfn_set_layout, tfn_set_option, tfn_stats, tfn_status_string,
                   tfn_version, tfn_auto_variant, tfn_estimate_u16, tfn_estimate_host_u16, tfn_estimate_points,
                   tfn_set_filter_weights, tfn_plane_fit, STAT_KEYS,
                   LIB_PATH)
 
-__all__ = ["Estimator", "TfnError", "stats", "debug_phi8", "lib", "LIB_PATH", "ABI_SYMBOLS", "STAT_KEYS"]
+__all__ = ["Estimator", "decode_oct16", "TfnError", "stats", "debug_phi8", "lib", "LIB_PATH", "ABI_SYMBOLS", "STAT_KEYS"]

@@ -35,7 +35,7 @@ struct tfn_ctx {
     int filter;
     int mode;
     int layout = TFN_LAYOUT_PLANAR;
-    int out_f16 = 0;                     // TFN_OPT_OUT_DTYPE
+    int out_kind = 0;                    // TFN_OPT_OUT_DTYPE: 0 fp32, 1 half, 2 oct16
     double kp = 1.0, k0 = 2.0;           // TFN_FILTER_CUSTOM weights (tfn_set_filter_weights)
     int kernel = tfn::TFN_KERNEL_AUTO;
     int strip_h = 0;
@@ -95,7 +95,9 @@ bool overlap(const void* a, size_t na, const void* b, size_t nb) {
 
 // bytes per sample in / per normal component out
 size_t in_bytes(int in_u16) { return in_u16 ? 2 : 4; }
-size_t out_bytes(const tfn_ctx* h) { return h->out_f16 ? 2 : 4; }
+// bytes per output pixel (normals) and the alignment the strip kernel's vector stores need
+size_t out_px_bytes(const tfn_ctx* h) { return h->out_kind == 0 ? 12 : h->out_kind == 1 ? 6 : 4; }
+uintptr_t out_align(const tfn_ctx* h) { return h->out_kind == 0 ? 15 : h->out_kind == 1 ? 7 : 15; }
 
 int validate(tfn_handle h, const void* in, int in_u16, int batch, int H, int W, const void* out) {
     if (!h) return TFN_ERR_INVALID_ARGUMENT;
@@ -104,9 +106,9 @@ int validate(tfn_handle h, const void* in, int in_u16, int batch, int H, int W, 
     if (!in || !out) return TFN_ERR_INVALID_ARGUMENT;
     const unsigned long long px = (unsigned long long)batch * (unsigned long long)H * (unsigned long long)W;
     if (px > (1ull << 60) / 12) return TFN_ERR_INVALID_ARGUMENT;
-    const size_t ib = in_bytes(in_u16), ob = out_bytes(h);
+    const size_t ib = in_bytes(in_u16), ob = h->out_kind == 0 ? 4 : 2;
     if (((uintptr_t)in & (ib - 1)) || ((uintptr_t)out & (ob - 1))) return TFN_ERR_INVALID_ARGUMENT;
-    if (overlap(in, px * ib, out, px * 3 * ob)) return TFN_ERR_INVALID_ARGUMENT;
+    if (overlap(in, px * ib, out, px * out_px_bytes(h))) return TFN_ERR_INVALID_ARGUMENT;
     return TFN_OK;
 }
 
@@ -116,7 +118,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
     a.in = in;
     a.out = out;
     a.in_u16 = in_u16;
-    a.out_f16 = h->out_f16;
+    a.out_kind = h->out_kind;
     a.pts = pts;
     a.pscale = (float)pscale;
     a.ifx = (float)(1.0 / h->K.fx);
@@ -134,7 +136,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
     // strip kernel: 4-sample vectors in and 4-component vectors out (16 B fp32, 8 B for
     // uint16 / half), and (frame, strip-row, strip-col) items indexed in 32 bits
     const long long max_items = (long long)((W + TFN_STRIP_COLS - 1) / TFN_STRIP_COLS) * ((H + 3) / 4) * (long long)batch;
-    const uintptr_t in_al = 4 * in_bytes(in_u16) - 1, out_al = 4 * out_bytes(h) - 1;
+    const uintptr_t in_al = 4 * in_bytes(in_u16) - 1, out_al = out_align(h);
     const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & in_al) == 0) && (((uintptr_t)out & out_al) == 0) &&
                           (((uintptr_t)pts & 15) == 0) && max_items < (1LL << 31);
     int kernel = h->kernel;
@@ -287,8 +289,8 @@ TFN_API int tfn_set_option(tfn_handle h, int option, long long value) {
         h->dynamic = value ? 1 : 0;
         return TFN_OK;
     case TFN_OPT_OUT_DTYPE:
-        if (value != TFN_OUT_F32 && value != TFN_OUT_F16) return TFN_ERR_INVALID_ARGUMENT;
-        h->out_f16 = (int)value;
+        if (value != TFN_OUT_F32 && value != TFN_OUT_F16 && value != TFN_OUT_OCT16) return TFN_ERR_INVALID_ARGUMENT;
+        h->out_kind = (int)value;
         return TFN_OK;
     default:
         return TFN_ERR_INVALID_ARGUMENT;
@@ -336,7 +338,7 @@ TFN_API int tfn_estimate_points(tfn_handle h, const void* input, int input_kind,
     if (!out_points || ((uintptr_t)out_points & 3)) return TFN_ERR_INVALID_ARGUMENT;
     const size_t px = (size_t)batch * H * W;
     if (overlap(out_points, px * 12, input, px * in_bytes(u16)) ||
-        overlap(out_points, px * 12, out_normals, px * 3 * out_bytes(h)))
+        overlap(out_points, px * 12, out_normals, px * out_px_bytes(h)))
         return TFN_ERR_INVALID_ARGUMENT;
     return run(h, input, u16, disp, batch, H, W, (cudaStream_t)stream, out_normals, out_points, scale);
 }
@@ -352,7 +354,7 @@ int host_run(tfn_handle h, const void* host_in, int in_u16, bool disp, int batch
     if (!host_in || !host_out) return TFN_ERR_INVALID_ARGUMENT;
     const size_t fpx = (size_t)H * (size_t)W;
     if ((unsigned long long)batch * fpx > (1ull << 60) / 12) return TFN_ERR_INVALID_ARGUMENT;
-    const size_t fin = fpx * in_bytes(in_u16), fout = fpx * 3 * out_bytes(h);
+    const size_t fin = fpx * in_bytes(in_u16), fout = fpx * out_px_bytes(h);
     std::lock_guard<std::mutex> lock(h->ws_mu);
     Workspace& ws = h->ws;
     size_t chunk = (48u << 20) / fin;

@@ -17,6 +17,7 @@
 
 #include "tfn_device.cuh"
 #include "tfn_kernels.h"
+#include "tfn_strip.cuh"      // oct16 (the normal encoding shared with the strip kernel)
 
 namespace tfn {
 
@@ -35,7 +36,12 @@ __global__ void __launch_bounds__(256) tfn_pixel_kernel(KernelArgs p) {
     const long long pix = (long long)v * p.W + u;
     const long long i0 = p.layout == 0 ? b * 3 * HW + pix : (b * HW + pix) * 3;
     const long long st = p.layout == 0 ? HW : 1;
-    if (p.out_f16) {
+    if (p.out_kind == 2) {
+        const unsigned w = oct16(n.x, n.y, n.z);
+        short* o = reinterpret_cast<short*>(p.out) + (p.layout == 0 ? b * 2 * HW + pix : (b * HW + pix) * 2);
+        o[0] = (short)(w & 0xffffu);
+        o[p.layout == 0 ? HW : 1] = (short)(w >> 16);
+    } else if (p.out_kind == 1) {
         __half* o = reinterpret_cast<__half*>(p.out) + i0;
         o[0] = __float2half_rn(n.x); o[st] = __float2half_rn(n.y); o[2 * st] = __float2half_rn(n.z);
     } else {

@@ -23,9 +23,10 @@ enum InDtype { TFN_IN_F32 = 0, TFN_IN_U16 = 1 };
 
 struct KernelArgs {
     const void* in;      // [B,H,W] depth or disparity: fp32, or uint16 depth codes (in_u16)
-    void* out;           // [B,3,H,W] (layout 0) or [B,H,W,3] (layout 1): fp32, or half (out_f16)
+    void* out;           // normals, layout 0 planar / 1 packed: fp32 or half [B,3,H,W] / [B,H,W,3],
+                         // or octahedral int16 pairs [B,2,H,W] / [B,H,W,2] (out_kind)
     int in_u16;
-    int out_f16;
+    int out_kind;        // 0 fp32, 1 half, 2 oct16 (TFN_OPT_OUT_DTYPE)
     long long B;
     int H, W;
     float fx, fy;        // n' = (fx g_u, fy g_v, n_z)   (Eq. 18)

@@ -50,7 +50,7 @@ struct StripCtx {
     float fx, fy;
     float a[4];        // u - u0 of the 4 columns
     int* fired;        // AUTO probe: += 1 per row step that needed the special path
-    bool f16;          // normals stored as IEEE half (N1), else fp32
+    int outk;          // normal encoding: 0 fp32, 1 IEEE half, 2 octahedral int16 pair (N1)
     float* pts;        // N3: this lane's point-cloud output (column cm) of the item's frame, or nullptr
     float pscale, ifx, ify;   // Z = pscale * sample (depth) or pscale / d (disparity); 1/fx, 1/fy
     Wts wt;            // CUSTOM filter weights
@@ -142,6 +142,45 @@ __device__ __forceinline__ void st2(float* p, float a, float b) {
 }
 __device__ __forceinline__ void st2h(void* p, float a, float b) {
     __stcs(reinterpret_cast<unsigned*>(p), h2(a, b));
+}
+// N1 octahedral encoding of a unit normal in two int16 snorms (4 B/pixel), camera hemisphere
+// (n_z <= 0) in the inner diamond: encode (n_x, n_y, -n_z) by the standard octahedral map,
+// fold the far hemisphere, round to nearest of 32767 steps (the FFMA against 1.5 * 2^23 puts
+// the rounded integer in the low mantissa bits: no conversion instruction).  NaN (invalid)
+// -> the sentinel pair (-32768, -32768), which the encoder never produces otherwise.
+__device__ __forceinline__ unsigned oct16(float x, float y, float z) {
+    const float zz = -z;
+    const float inv = rcp_approx(fabsf(x) + fabsf(y) + fabsf(zz));
+    float px = x * inv, py = y * inv;
+    if (zz < 0.f) {
+        const float ax = fabsf(px), ay = fabsf(py);
+        px = copysignf(1.f - ay, px);
+        py = copysignf(1.f - ax, py);
+    }
+    px = fminf(fmaxf(px, -1.f), 1.f);
+    py = fminf(fmaxf(py, -1.f), 1.f);
+    const unsigned qx = __float_as_uint(__fmaf_rn(px, 32767.f, 12582912.f)) - 0x4B400000u;
+    const unsigned qy = __float_as_uint(__fmaf_rn(py, 32767.f, 12582912.f)) - 0x4B400000u;
+    const unsigned w = (qx & 0xffffu) | (qy << 16);
+    return isnan(x) ? 0x80008000u : w;
+}
+__device__ __forceinline__ void store_oct(short* o, long long plane, const float* x, const float* y,
+                                          const float* z, bool planar) {
+    unsigned w[4];
+#pragma unroll
+    for (int i = 0; i < PPL; ++i) w[i] = oct16(x[i], y[i], z[i]);
+    if (planar) {      // u plane, v plane: PPL shorts each
+        if (PPL == 4) {
+            __stcs(reinterpret_cast<uint2*>(o), make_uint2(__byte_perm(w[0], w[1], 0x5410), __byte_perm(w[2], w[3], 0x5410)));
+            __stcs(reinterpret_cast<uint2*>(o + plane), make_uint2(__byte_perm(w[0], w[1], 0x7632), __byte_perm(w[2], w[3], 0x7632)));
+        } else {
+            __stcs(reinterpret_cast<unsigned*>(o), __byte_perm(w[0], w[1], 0x5410));
+            __stcs(reinterpret_cast<unsigned*>(o + plane), __byte_perm(w[0], w[1], 0x7632));
+        }
+    } else {           // packed (u, v) per pixel
+        if (PPL == 4) __stcs(reinterpret_cast<uint4*>(o), make_uint4(w[0], w[1], w[2], w[3]));
+        else __stcs(reinterpret_cast<uint2*>(o), make_uint2(w[0], w[1]));
+    }
 }
 // one component plane (or the packed triples) of the lane's PPL pixels
 __device__ __forceinline__ void store_planar(float* o, const float* x) {
@@ -334,11 +373,14 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
             }
         }
     }
-    // ---- store (16-B / 8-B aligned: W % 4 == 0, c0 % 4 == 0).  OUT: 0 fp32, 1 half, 2 the
-    //      handle's choice at run time (general variant); the point cloud is general-only ----
+    // ---- store (16-B / 8-B aligned: W % 4 == 0, c0 % 4 == 0).  OUT: 0 fp32, 1 half, 3 oct16,
+    //      2 the handle's choice at run time (general variant); points are general-only ----
     if (c.okm) {
-        const bool f16 = (OUT == 2) ? c.f16 : (OUT == 1);
-        if (!f16) {
+        const int kind = (OUT == 2) ? c.outk : (OUT == 3 ? 2 : OUT);
+        if (kind == 2) {
+            short* o = reinterpret_cast<short*>(out) + v * c.W * (LAYOUT == 0 ? 1 : 2);
+            store_oct(o, HW, nx, ny, nz, LAYOUT == 0);
+        } else if (kind == 0) {
             float* o = reinterpret_cast<float*>(out) + v * c.W * (LAYOUT == 0 ? 1 : 3);
             if (LAYOUT == 0) {
                 store_planar(o, nx);
@@ -436,9 +478,10 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
     c.u0 = p.u0; c.v0 = p.v0;
     c.fired = p.fired;
     c.wt.kp = p.kp; c.wt.k0 = p.k0;
-    c.f16 = (OUT == 2) ? p.out_f16 != 0 : OUT == 1;
+    c.outk = (OUT == 2) ? p.out_kind : (OUT == 3 ? 2 : OUT);
     c.pscale = p.pscale; c.ifx = p.ifx; c.ify = p.ify;
-    const int es = c.f16 ? 2 : 4;          // bytes per output component
+    const int cb = c.outk == 0 ? 4 : 2;          // bytes per stored component
+    const int nc = c.outk == 2 ? 2 : 3;          // stored components per pixel
 
     // first item static, the rest claimed from a work counter (load balance: strips with
     // holes or sky cost more or less than others); static striding without a counter
@@ -464,7 +507,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
             if (c0 == 0) colmask |= 1u;
             if (c0 + PPL - 1 == p.W - 1) colmask |= 1u << (PPL - 1);
         }
-        char* out = reinterpret_cast<char*>(p.out) + es * (fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm));
+        char* out = reinterpret_cast<char*>(p.out) + cb * (fb * nc * HW + (LAYOUT == 0 ? (long long)c.cm : (long long)nc * c.cm));
         c.pts = p.pts ? p.pts + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm) : nullptr;
 
         strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS, OUT>(c, out, HW, p.layout, colmask, y0, y1);

@@ -5,8 +5,8 @@
 // {planar, packed} x {general} (integer-quantized depth makes dZ = 0 common, so the
 // fast variant's special path would run on most row steps); and the general variant with
 // the fused point cloud (N3) for every input.  The fast variant is compiled per normal
-// dtype (fp32 / half); the general one reads the dtype at run time; points run the general
-// variant (same bits).
+// encoding (fp32 / half / oct16); the general one reads it at run time; points run the
+// general variant (same bits).
 #pragma once
 #include "tfn_device.cuh"
 #include "tfn_kernels.h"
@@ -23,8 +23,9 @@ static cudaError_t launch_l(const KernelArgs& a, int grid, cudaStream_t st) {
 
 template <int F, int MODE, bool DISP>
 static cudaError_t launch_fast(const KernelArgs& a, int grid, cudaStream_t st) {
-    return a.out_f16 ? launch_l<F, MODE, DISP, 0, float, false, 1>(a, grid, st)
-                     : launch_l<F, MODE, DISP, 0, float, false, 0>(a, grid, st);
+    return a.out_kind == 1 ? launch_l<F, MODE, DISP, 0, float, false, 1>(a, grid, st)
+         : a.out_kind == 2 ? launch_l<F, MODE, DISP, 0, float, false, 3>(a, grid, st)
+                           : launch_l<F, MODE, DISP, 0, float, false, 0>(a, grid, st);
 }
 
 // variant 0 = fast, 1 = general; uint16 input and points always run general

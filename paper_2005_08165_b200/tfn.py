@@ -25,7 +25,7 @@ FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3, "custom": 4}
 MODES = {"mean": 0, "median": 1}
 LAYOUTS = {"planar": 0, "packed": 1}
 KERNELS = {"auto": 0, "pixel": 1, "strip": 2, "general": 3}
-OUT_DTYPES = {"f32": 0, "f16": 1}
+OUT_DTYPES = {"f32": 0, "f16": 1, "oct16": 2}
 OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_DYNAMIC, OPT_OUT_DTYPE = 0, 1, 2, 3, 4
 
 # every symbol include/tfn.h declares (tests/test_abi.py checks the export table)
@@ -232,7 +232,8 @@ class Estimator:
         self.K = K.as_tuple() if hasattr(K, "as_tuple") else tuple(float(x) for x in K)
         self.filter, self.nz_mode, self.layout = filter, nz_mode, layout
         self.out_dtype = out_dtype
-        self._odt = torch.float16 if out_dtype == "f16" else torch.float32
+        self._odt = {"f32": torch.float32, "f16": torch.float16, "oct16": torch.int16}[out_dtype]
+        self._nc = 2 if out_dtype == "oct16" else 3        # stored components per pixel
         # filter: a name, or the (kp, k0) weights of [kp k0 kp]^T (x) [-1 0 1] (TFN_FILTER_CUSTOM)
         custom = isinstance(filter, (tuple, list))
         self.h = tfn_create(self.K, FILTERS["custom" if custom else filter], MODES[nz_mode])
@@ -245,12 +246,14 @@ class Estimator:
         tfn_set_option(self.h, OPT_DYNAMIC, int(dynamic))
         tfn_set_option(self.h, OPT_OUT_DTYPE, OUT_DTYPES[out_dtype])
 
+    def _shape(self, B, H, W):
+        return (B, self._nc, H, W) if self.layout == "planar" else (B, H, W, self._nc)
+
     def _out(self, B, H, W, like: torch.Tensor, out):
-        shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
         if out is None:
-            out = torch.empty(shape, dtype=self._odt, device=like.device)
+            out = torch.empty(self._shape(B, H, W), dtype=self._odt, device=like.device)
         _need(out, "out", device=like.is_cuda, dtype=self._odt)
-        if out.numel() != 3 * B * H * W:
+        if out.numel() != self._nc * B * H * W:
             raise TfnError(TFN_ERR_INVALID_ARGUMENT, "out has the wrong size")
         return out
 
@@ -330,9 +333,9 @@ class Estimator:
         B, H, W = _bhw(host_in)
         if out is None:
             shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
-            out = torch.empty(shape, dtype=self._odt, pin_memory=True)
+            out = torch.empty(self._shape(B, H, W), dtype=self._odt, pin_memory=True)
         _need(out, "out", device=False, dtype=self._odt)
-        if out.numel() != 3 * B * H * W:
+        if out.numel() != self._nc * B * H * W:
             raise TfnError(TFN_ERR_INVALID_ARGUMENT, "out has the wrong size")
         if u16:
             _check(tfn_estimate_host_u16(self.h, host_in.data_ptr(), baseline_times_f if baseline_times_f != 1.0
@@ -377,6 +380,26 @@ def debug_phi8(cand: torch.Tensor, nz_mode: str) -> Tuple[torch.Tensor, torch.Te
     _check(tfn_debug_phi8(cand.data_ptr(), n, MODES[nz_mode], out.data_ptr(), k.data_ptr(),
                           _stream_ptr(None)), "tfn_debug_phi8")
     return out, k
+
+
+def decode_oct16(q: torch.Tensor, layout: str = "planar") -> torch.Tensor:
+    """Unit normals (fp32, planar [B,3,H,W] or packed [B,H,W,3]) from TFN_OUT_OCT16 pairs
+    (include/tfn.h); the sentinel (-32768, -32768) decodes to NaN.  Plain torch ops."""
+    u, v = (q[:, 0], q[:, 1]) if layout == "planar" else (q[..., 0], q[..., 1])
+    bad = (u == -32768) & (v == -32768)
+    px = (u.float() / 32767.0).clamp(-1, 1)
+    py = (v.float() / 32767.0).clamp(-1, 1)
+    z = 1.0 - px.abs() - py.abs()
+    sx = torch.where(px >= 0, 1.0, -1.0)
+    sy = torch.where(py >= 0, 1.0, -1.0)
+    fx = torch.where(z < 0, (1.0 - py.abs()) * sx, px)
+    fy = torch.where(z < 0, (1.0 - px.abs()) * sy, py)
+    vec = torch.stack([fx, fy, z], dim=1 if layout == "planar" else -1)
+    vec = vec / vec.norm(dim=1 if layout == "planar" else -1, keepdim=True)
+    sign = torch.tensor([1.0, 1.0, -1.0], device=q.device)
+    n = vec * (sign.view(1, 3, 1, 1) if layout == "planar" else sign)
+    nan = torch.full_like(n, float("nan"))
+    return torch.where((bad.unsqueeze(1) if layout == "planar" else bad.unsqueeze(-1)), nan, n)
 
 
 STAT_KEYS = ("sum_psi_micro_deg", "m", "n_le_10", "n_le_20", "n_le_30", "n_valid_est", "n_valid_gt",

@@ -139,4 +139,38 @@ def test_u16_host_path_and_errors(tfn):
     torch.cuda.synchronize()
     assert same_bits(out.cpu(), dev)             # the scale cancels: identical bits
     with pytest.raises(T.TfnError):
-        T.tfn_set_option(est.h, T.OPT_OUT_DTYPE, 2)
+        T.tfn_set_option(est.h, T.OPT_OUT_DTYPE, 3)
+
+
+def test_oct16_normals(tfn):
+    """TFN_OUT_OCT16 (4 B/pixel): the decoded direction is within 0.005 deg of the fp32
+    normal (snorm16 steps of 1/32767 on the octahedral map), the invalid mask maps to the
+    (-32768, -32768) sentinel, and every kernel and layout writes the same bits; uint16
+    input works too (2 + 4 = 6 B/pixel end to end)"""
+    sc = ts.random_scenes(2, ts.K_VGA, 480, 640, seed=13, holes=True, salt=0.005)
+    z = ts.render(sc, ts.K_VGA, 480, 640).depth
+    from oracle import metrics
+    ref32 = run_f32(tfn, z.numpy(), ts.K_VGA, "sobel", "median").numpy()
+    base = None
+    for layout in ("planar", "packed"):
+        for kernel in ("auto", "strip", "general", "pixel"):
+            q = run_f32(tfn, z.numpy(), ts.K_VGA, "sobel", "median", kernel=kernel, layout=layout,
+                        out_dtype="oct16")
+            assert q.dtype == torch.int16 and q.shape == ((2, 2, 480, 640) if layout == "planar" else (2, 480, 640, 2))
+            qp = q if layout == "planar" else q.permute(0, 3, 1, 2).contiguous()
+            if base is None:
+                base = qp
+            assert torch.equal(qp, base), (layout, kernel)
+    n = tfn.decode_oct16(base).numpy()
+    ok = np.all(np.isfinite(ref32), 1)
+    assert np.array_equal(ok, np.all(np.isfinite(n), 1))
+    assert ((base[:, 0] == -32768) & (base[:, 1] == -32768)).numpy().sum() == (~ok).sum()
+    a = metrics.angular_error_deg(np.moveaxis(n, 1, -1)[ok], np.moveaxis(ref32, 1, -1)[ok])
+    assert a.max() < 0.005, a.max()
+    codes = mm_codes(frames=2, seed=14)
+    qu = run_u16(tfn, codes, ts.K_VGA, "fd", "median", out_dtype="oct16")
+    ru = run_u16(tfn, codes, ts.K_VGA, "fd", "median").numpy()
+    nu = tfn.decode_oct16(qu).numpy()
+    oku = np.all(np.isfinite(ru), 1)
+    assert np.array_equal(oku, np.all(np.isfinite(nu), 1))
+    assert metrics.angular_error_deg(np.moveaxis(nu, 1, -1)[oku], np.moveaxis(ru, 1, -1)[oku]).max() < 0.005
