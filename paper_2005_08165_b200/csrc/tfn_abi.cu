@@ -141,6 +141,11 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
                           (((uintptr_t)pts & 15) == 0) && max_items < (1LL << 31);
     int kernel = h->kernel;
     bool probe = false;
+    // CUDA-graph capture: no host-side event query or read-back while capturing (the AUTO
+    // choice made so far is baked into the graph; the work counter memset is a graph node)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) { cudaGetLastError(); cap = cudaStreamCaptureStatusNone; }
+    const bool capturing = cap != cudaStreamCaptureStatusNone;
     if (kernel == tfn::TFN_KERNEL_AUTO) {
         if (!strip_ok) {
             kernel = tfn::TFN_KERNEL_PIXEL;
@@ -148,7 +153,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
             kernel = tfn::TFN_KERNEL_STRIP_GENERAL;     // the only strip variant built for these
         } else {
             std::lock_guard<std::mutex> lk(h->auto_mu);
-            if (h->fb_pending && cudaEventQuery(h->fb_ev) == cudaSuccess) {
+            if (!capturing && h->fb_pending && cudaEventQuery(h->fb_ev) == cudaSuccess) {
                 const double rate = h->fb_steps > 0 ? *h->fb_host / h->fb_steps : 0.0;
                 if (rate > TFN_AUTO_GENERAL_ABOVE) h->auto_general = 1;
                 else if (rate < TFN_AUTO_FAST_BELOW) h->auto_general = 0;
@@ -156,9 +161,9 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
             }
             cudaGetLastError();           // a not-ready query is not an error
             const unsigned n = h->auto_calls++;
-            const bool use_general = h->auto_general && (n % TFN_AUTO_PROBE_GENERAL) != 0;
+            const bool use_general = h->auto_general && (capturing || (n % TFN_AUTO_PROBE_GENERAL) != 0);
             kernel = use_general ? tfn::TFN_KERNEL_STRIP_GENERAL : tfn::TFN_KERNEL_STRIP;
-            probe = !use_general && h->fb_host && !h->fb_pending &&
+            probe = !capturing && !use_general && h->fb_host && !h->fb_pending &&
                     (h->auto_general || (n % TFN_AUTO_PROBE_FAST) == 0);
         }
     }

@@ -488,3 +488,28 @@ def test_custom_weights_reproduce_named_kernels(tfn, random8):
             T.tfn_set_filter_weights(est.h, *bad)
     with pytest.raises(T.TfnError):
         T.tfn_set_filter_weights(tfn.Estimator(ts.K_VGA, "sobel", "median").h, 1.0, 2.0)
+
+
+def test_cuda_graph_capture(tfn, cfg1, random8):
+    """the ABI is capture-safe (no host sync / event query while a stream captures): a
+    CUDA graph of one estimate call replays to the same bits, also after the input buffer
+    is refilled in place; AUTO's choice at capture time is baked in"""
+    x = random8.depth[:2].cuda().contiguous()
+    est = tfn.Estimator(ts.K_VGA, "sobel", "median")
+    ref = est.estimate(x).clone()
+    out = torch.empty_like(ref)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            est.estimate(x, out=out, stream=side)
+    torch.cuda.current_stream().wait_stream(side)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int32), ref.view(torch.int32))
+    x.copy_(random8.depth[2:4].cuda())
+    g.replay()
+    torch.cuda.synchronize()
+    ref2 = est.estimate(x)
+    assert torch.equal(out.view(torch.int32), ref2.view(torch.int32))
