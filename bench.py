@@ -459,14 +459,14 @@ def main():
     if not args.no_e2e and not args.profile and not streaming_cfg:
         hin = x.cpu().pin_memory()
         hout = torch.empty(out.shape, dtype=odt, pin_memory=True)
-        bf = DEPTH_SCALE if cfg.get("u16") else BASELINE_F * BASELINE_B
-        est.estimate_host(hin, is_disparity=cfg["disp"], baseline_times_f=bf, out=hout)
+        bf = BASELINE_F * BASELINE_B
+        est.estimate_host(hin, is_disparity=cfg["disp"], baseline_times_f=bf, out=hout, depth_scale=DEPTH_SCALE)
         if pg:
             pg.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            est.estimate_host(hin, is_disparity=cfg["disp"], baseline_times_f=bf, out=hout)
+            est.estimate_host(hin, is_disparity=cfg["disp"], baseline_times_f=bf, out=hout, depth_scale=DEPTH_SCALE)
         dt = time.perf_counter() - t0
         # wall clock of a blocking host->device->host call; max over ranks
         tt = torch.tensor([dt], dtype=torch.float64, device=dev)

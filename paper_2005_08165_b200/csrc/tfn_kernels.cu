@@ -1,15 +1,11 @@
 // tfn_kernels.cu — the per-pixel 3F2N kernel and the launch dispatch for sm_100a (the strip
 // kernel's instantiations live in tfn_strip_<filter>.cu).
 //
-//   tfn_strip_kernel   the production kernel (W % 4 == 0, 16-B aligned buffers):
-//                      one warp owns a 128-column x R-row strip; each lane owns 4
-//                      adjacent columns and walks down the strip keeping a rolling
-//                      3-row register window (sanitized Z, fp64 1/Z, gradient
-//                      partial sums, shared pair reciprocals).  One LDG.128 + two
-//                      halo LDG.32 per lane-row in, three STG.128 per lane-row out:
-//                      16 B/pixel of HBM traffic (4 read + 12 written).
-//   tfn_pixel_kernel   one thread per pixel, any W; same arithmetic (bit-identical
-//                      results, checked by tests/test_gpu_parity.py).
+//   tfn_strip_kernel   the production kernel (tfn_strip.cuh; W % 4 == 0, vector-aligned
+//                      buffers): warp strips with a rolling 3-row register window,
+//                      16 B/pixel of HBM traffic for fp32 in / fp32 normals out.
+//   tfn_pixel_kernel   one thread per pixel, any W / alignment; the same device
+//                      routines (bit-identical results, tests/test_gpu_parity.py).
 //
 // Both evaluate PAPER.md Eq. 13-21 as described in tfn_device.cuh and
 // DESIGN.md §2; neither shares code with oracle/.

@@ -1,23 +1,30 @@
-// tfn_strip.cuh — the production 3F2N kernel (included by tfn_kernels.cu).
+// tfn_strip.cuh — the production 3F2N kernel (instantiated per filter in
+// tfn_strip_<filter>.cu via tfn_strip_inst.cuh).
 //
-// Geometry.  One warp owns a strip of 128 columns x strip_h rows of one frame; each
-// lane owns 4 adjacent columns c0..c0+3 and walks down the strip with a rolling
-// window of three row "slots" (rows v-1, v, v+1).  The row loop is unrolled by 3
-// and the slots rotate by renaming (no register copies).  Per lane-row: one
-// LDG.128 + two halo LDG.32 in (clamped addresses, never out of bounds), three
-// STG.128 out.  Persistent grid: warps stride over (frame, strip-row, strip-col).
+// Geometry.  One warp owns a strip of 32*PPL columns (PPL = 4: 128) x strip_h rows of one
+// frame; each lane owns PPL adjacent columns and walks down the strip with a rolling
+// window of three row "slots" (rows v-1, v, v+1).  The row loop is unrolled by 3 and the
+// slots rotate by renaming (no register copies).  Per lane-row: one LDG.128 (fp32) or
+// LDG.64 (uint16) + two predicated halo loads in, three STG.128 (fp32) / STG.64 (half) /
+// one or two vector stores (oct16) out, loads prefetched three rows ahead.  Persistent
+// grid; strips handed out by an atomic work counter (dynamic scheduling).
 //
 // Arithmetic (bit-identical to tfn_pixel_kernel, see tfn_device.cuh):
-//   fp64:  w = 1/z (correctly rounded), D_h, D_v, g_u, g_v in the oracle's order,
+//   fp64:  w = 1/z (faithful, ~2^-66), D_h, D_v, g_u, g_v in the oracle's order,
 //          s = g_u + g_v, t = g_v - g_u, rounded once to fp32;
 //   fp32:  one MUFU reciprocal per neighbour PAIR (shared by both pixels of the pair),
-//          rho, tau = m * rho, Phi, n_z, normalise, orient — the per-pixel tail in
-//          packed FMUL2/FFMA2/FADD2 over pixel pairs (0,1), (2,3).
-// Fast path: all 8 candidates finite and Phi != 0 (no skips, no flat rule, no
-// orientation tie, valid pixel).  Anything else ("special": holes, invalid samples,
-// dZ == 0, flat, ties) takes the general per-pixel code behind ONE warp vote per
-// row step.  Border pixels are never special: their out-of-image taps are NaN, so the
-// fast path already writes the canonical NaN.
+//          tau = fma(m Z_c, R, +-m), Phi (24-op median network / mean), n_z, normalise,
+//          orient — packed FMUL2/FFMA2/FADD2 over pixel pairs (0,1), (2,3).
+// Two variants (KV):
+//   fast (0):    all 8 candidates finite and Phi != 0 (no skips, no flat rule, no
+//                orientation tie, valid pixel) in registers; anything else ("special":
+//                holes, invalid samples, dZ == 0, flat, ties) runs the exact per-pixel
+//                routine behind ONE warp vote per row step.  Border pixels are never
+//                special: their out-of-image taps are NaN, so the fast path already
+//                writes the canonical NaN.
+//   general (1): no special path — invalid samples get NaN fp64 x (F2F), skipped
+//                candidates are padded in registers (phi_any), flat / none / ties /
+//                invalid resolved by finish_tail: the per-pixel kernel's code, inline.
 #pragma once
 
 #ifndef TFN_STRIP_PPL

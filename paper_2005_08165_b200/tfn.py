@@ -322,25 +322,23 @@ class Estimator:
         return out
 
     def estimate_host(self, host_in: torch.Tensor, is_disparity: bool = False, baseline_times_f: float = 1.0,
-                      out: Optional[torch.Tensor] = None,
-                      stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
-        """Host buffers in and out (pinned for full overlap); blocking.  host_in fp32 (depth or
-        disparity) or uint16 depth codes (baseline_times_f is then the depth scale)."""
+                      out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None,
+                      depth_scale: float = 1e-3) -> torch.Tensor:
+        """Host buffers in and out (pinned for full overlap); blocking.  host_in fp32 (depth, or
+        disparity with baseline_times_f = f * t_c) or uint16 depth codes (Z = code * depth_scale)."""
         u16 = host_in.dtype == torch.uint16
         _need(host_in, "host_in", device=False, dtype=torch.uint16 if u16 else torch.float32)
         if host_in.is_cuda:
             raise TfnError(TFN_ERR_INVALID_ARGUMENT, "host_in must be a CPU tensor")
         B, H, W = _bhw(host_in)
         if out is None:
-            shape = (B, 3, H, W) if self.layout == "planar" else (B, H, W, 3)
             out = torch.empty(self._shape(B, H, W), dtype=self._odt, pin_memory=True)
         _need(out, "out", device=False, dtype=self._odt)
         if out.numel() != self._nc * B * H * W:
             raise TfnError(TFN_ERR_INVALID_ARGUMENT, "out has the wrong size")
         if u16:
-            _check(tfn_estimate_host_u16(self.h, host_in.data_ptr(), baseline_times_f if baseline_times_f != 1.0
-                                         else 1e-3, B, H, W, out.data_ptr(), _stream_ptr(stream)),
-                   "tfn_estimate_host_u16")
+            _check(tfn_estimate_host_u16(self.h, host_in.data_ptr(), depth_scale, B, H, W, out.data_ptr(),
+                                         _stream_ptr(stream)), "tfn_estimate_host_u16")
         else:
             _check(tfn_estimate_host(self.h, host_in.data_ptr(), int(is_disparity), baseline_times_f, B, H, W,
                                      out.data_ptr(), _stream_ptr(stream)), "tfn_estimate_host")

@@ -128,7 +128,7 @@ def test_u16_host_path_and_errors(tfn):
     codes = mm_codes(frames=5, seed=12)
     est = tfn.Estimator(ts.K_VGA, "sobel", "median", out_dtype="f16")
     dev = est.estimate(torch.from_numpy(codes).cuda(), depth_scale=SCALE).cpu()
-    host = est.estimate_host(torch.from_numpy(codes).pin_memory(), baseline_times_f=SCALE)
+    host = est.estimate_host(torch.from_numpy(codes).pin_memory(), depth_scale=SCALE)
     assert host.dtype == torch.float16 and same_bits(host, dev)
     # depth_scale must be finite and > 0 (validated, then unused)
     x = torch.from_numpy(codes).cuda()
