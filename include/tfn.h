@@ -189,7 +189,9 @@ int tfn_debug_phi8(const float* cand_dev, long long n, int nz_mode, float* out_d
  * (INVALID_ARGUMENT otherwise).  Asynchronous on stream. */
 int tfn_debug_sol(const float* in_dev, int batch, int H, int W, void* stream, float* out_dev);
 
-/* Release a handle (and its workspace).  NULL is OK. */
+/* Release a handle (and its workspace, work counters and AUTO read-back word).  NULL is
+ * OK.  Frees device memory with cudaFree (which waits for the device), so work already
+ * submitted with h completes first; no call may use h afterwards. */
 int tfn_destroy(tfn_handle h);
 
 /* Static string for a status code. */
