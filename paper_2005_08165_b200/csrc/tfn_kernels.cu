@@ -59,18 +59,27 @@ __global__ void __launch_bounds__(256) tfn_pixel_kernel(KernelArgs p) {
 // dispatch
 // ------------------------------------------------------------------------------------
 template <int F, int MODE>
-static cudaError_t launch_pixel(const KernelArgs& a, bool disp, cudaStream_t st) {
-    dim3 blk(32, 8, 1);
-    dim3 grd((a.W + 31) / 32, (a.H + 7) / 8, (unsigned)a.B);
-    if (a.in_u16) {
-        if (disp) return cudaErrorInvalidValue;
-        tfn_pixel_kernel<F, MODE, false, unsigned short><<<grd, blk, 0, st>>>(a);
-    } else if (disp) {
-        tfn_pixel_kernel<F, MODE, true, float><<<grd, blk, 0, st>>>(a);
-    } else {
-        tfn_pixel_kernel<F, MODE, false, float><<<grd, blk, 0, st>>>(a);
+static cudaError_t launch_pixel(const KernelArgs& a0, bool disp, cudaStream_t st) {
+    if (a0.in_u16 && disp) return cudaErrorInvalidValue;
+    // frames on grid z, at most 65535 per launch: larger batches go in chunks
+    const long long HW = (long long)a0.H * a0.W;
+    const size_t in_b = a0.in_u16 ? 2 : 4;
+    const size_t out_px = a0.out_kind == 0 ? 12 : a0.out_kind == 1 ? 6 : 4;
+    for (long long b0 = 0; b0 < a0.B; b0 += 65535) {
+        KernelArgs a = a0;
+        a.B = (a0.B - b0 < 65535) ? a0.B - b0 : 65535;
+        a.in = static_cast<const char*>(a0.in) + b0 * HW * in_b;
+        a.out = static_cast<char*>(a0.out) + b0 * HW * out_px;
+        if (a0.pts) a.pts = a0.pts + b0 * 3 * HW;
+        dim3 blk(32, 8, 1);
+        dim3 grd((a.W + 31) / 32, (a.H + 7) / 8, (unsigned)a.B);
+        if (a.in_u16) tfn_pixel_kernel<F, MODE, false, unsigned short><<<grd, blk, 0, st>>>(a);
+        else if (disp) tfn_pixel_kernel<F, MODE, true, float><<<grd, blk, 0, st>>>(a);
+        else tfn_pixel_kernel<F, MODE, false, float><<<grd, blk, 0, st>>>(a);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
     }
-    return cudaGetLastError();
+    return cudaSuccess;
 }
 
 template <int F>

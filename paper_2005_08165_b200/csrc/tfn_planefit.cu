@@ -174,11 +174,17 @@ __global__ void __launch_bounds__(256) tfn_planefit_kernel(const float* __restri
 
 cudaError_t launch_planefit(const float* depth, float* out, long long B, int H, int W, double fx, double fy,
                             double u0, double v0, int layout, int method, cudaStream_t st) {
-    dim3 blk(32, 8, 1);
-    dim3 grd((W + 31) / 32, (H + 7) / 8, (unsigned)B);
-    if (method == 0) tfn_planefit_kernel<0><<<grd, blk, 0, st>>>(depth, out, H, W, fx, fy, u0, v0, layout);
-    else tfn_planefit_kernel<1><<<grd, blk, 0, st>>>(depth, out, H, W, fx, fy, u0, v0, layout);
-    return cudaGetLastError();
+    const long long HW = (long long)H * W;
+    for (long long b0 = 0; b0 < B; b0 += 65535) {          // frames on grid z, <= 65535 per launch
+        const long long n = (B - b0 < 65535) ? B - b0 : 65535;
+        dim3 blk(32, 8, 1);
+        dim3 grd((W + 31) / 32, (H + 7) / 8, (unsigned)n);
+        if (method == 0) tfn_planefit_kernel<0><<<grd, blk, 0, st>>>(depth + b0 * HW, out + b0 * 3 * HW, H, W, fx, fy, u0, v0, layout);
+        else tfn_planefit_kernel<1><<<grd, blk, 0, st>>>(depth + b0 * HW, out + b0 * 3 * HW, H, W, fx, fy, u0, v0, layout);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace tfn

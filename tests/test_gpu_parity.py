@@ -513,3 +513,19 @@ def test_cuda_graph_capture(tfn, cfg1, random8):
     torch.cuda.synchronize()
     ref2 = est.estimate(x)
     assert torch.equal(out.view(torch.int32), ref2.view(torch.int32))
+
+
+def test_pixel_kernel_large_batch(tfn):
+    """more than 65535 frames (grid z limit) through the per-pixel kernel: chunked launches"""
+    B, H, W = 70000, 3, 5
+    z = torch.full((B, H, W), 2.0, device="cuda")
+    z[-1, 1, 1:4] = torch.tensor([2.0, 2.2, 2.4])
+    est = tfn.Estimator(ts.K_VGA, "fd", "median", kernel="pixel")
+    out = est.estimate(z)
+    torch.cuda.synchronize()
+    assert torch.equal(out[0, :, 1, 1], torch.tensor([0.0, 0.0, -1.0], device="cuda"))
+    assert torch.equal(out[65535, :, 1, 1], torch.tensor([0.0, 0.0, -1.0], device="cuda"))
+    assert not torch.equal(out[-1, :, 1, 2], out[0, :, 1, 2])
+    p = est.plane_fit(z, "pca")
+    torch.cuda.synchronize()
+    assert torch.isfinite(p[-1, :, 1, 1]).all() and torch.isnan(p[-1, :, 0, 0]).all()
