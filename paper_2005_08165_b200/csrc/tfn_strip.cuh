@@ -283,24 +283,39 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         const float2 xs = __fmul2_rn(ms, zc2), xt = __fmul2_rn(mt, zc2);
         float2 tau[8];
         float2 sum8;
-        if (DISP) {
+        if (MODE == MEAN) {
+            // mean numerator by neighbour-direction pairs (tfn_device.cuh, finish32): the
+            // +-m of opposite candidates cancel exactly, sum = sum_dir x_dir (R_a + R_b)
+            const float2 p23 = __fmul2_rn(xv, __fadd2_rn(f2(R[0][2], R[1][2]), f2(R[0][3], R[1][3])));
+            const float2 p67 = __fmul2_rn(xt, __fadd2_rn(f2(R[0][6], R[1][6]), f2(R[0][7], R[1][7])));
+            const float2 s0 = __ffma2_rn(xu, __fadd2_rn(f2(R[0][0], R[1][0]), f2(R[0][1], R[1][1])), p23);
+            const float2 s1 = __ffma2_rn(xs, __fadd2_rn(f2(R[0][4], R[1][4]), f2(R[0][5], R[1][5])), p67);
+            sum8 = __fadd2_rn(s0, s1);
+            if (GEN) {       // the general variant's k < 8 fallback needs the candidates
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float2 x = (k < 2) ? xu : (k < 4) ? xv : (k < 6) ? xs : xt;
+                    const float2 m = (k < 2) ? mu : (k < 4) ? mv : (k < 6) ? ms : mt;
+                    tau[k] = DISP ? __fmul2_rn(x, f2(R[0][k], R[1][k]))
+                                  : __ffma2_rn(x, f2(R[0][k], R[1][k]), (k & 1) ? f2(-m.x, -m.y) : m);
+                }
+            }
+        } else if (DISP) {
 #pragma unroll
             for (int k = 0; k < 8; k += 2) {
                 const float2 x = (k < 2) ? xu : (k < 4) ? xv : (k < 6) ? xs : xt;
                 tau[k] = __fmul2_rn(x, f2(R[0][k], R[1][k]));
             }
-            // finish32's explicit-FMA sum
+            // finish32's explicit-FMA sum (median: only its finiteness is used)
             const float2 s01 = __ffma2_rn(xu, f2(R[0][1], R[1][1]), tau[0]);
             const float2 s23 = __ffma2_rn(xv, f2(R[0][3], R[1][3]), tau[2]);
             const float2 s45 = __ffma2_rn(xs, f2(R[0][5], R[1][5]), tau[4]);
             const float2 s67 = __ffma2_rn(xt, f2(R[0][7], R[1][7]), tau[6]);
             sum8 = __fadd2_rn(__fadd2_rn(s01, s23), __fadd2_rn(s45, s67));
-            if (MODE == MEDIAN || GEN) {     // the general variant also needs every candidate
 #pragma unroll
-                for (int k = 1; k < 8; k += 2) {
-                    const float2 x = (k < 2) ? xu : (k < 4) ? xv : (k < 6) ? xs : xt;
-                    tau[k] = __fmul2_rn(x, f2(R[0][k], R[1][k]));
-                }
+            for (int k = 1; k < 8; k += 2) {
+                const float2 x = (k < 2) ? xu : (k < 4) ? xv : (k < 6) ? xs : xt;
+                tau[k] = __fmul2_rn(x, f2(R[0][k], R[1][k]));
             }
         } else {
 #pragma unroll

@@ -529,3 +529,26 @@ def test_pixel_kernel_large_batch(tfn):
     p = est.plane_fit(z, "pca")
     torch.cuda.synchronize()
     assert torch.isfinite(p[-1, :, 1, 1]).all() and torch.isnan(p[-1, :, 0, 0]).all()
+
+
+# ------------------------------------------------------------------ extreme ranges / intrinsics
+@pytest.mark.parametrize("scale", [1e-3, 1.0, 3e3])
+def test_extreme_depth_scales_and_occlusions(tfn, random8, scale):
+    """depth in millimetres-of-a-micro-scene up to kilometres, with occlusion steps of 100x
+    (near/far mixes inside one 3x3 window) and tiny / huge focal lengths: parity and the
+    three kernels bit-identical"""
+    z = random8.depth.numpy()[:2].astype(np.float64) * scale
+    rng = np.random.default_rng(int(scale * 1000) % 2**31)
+    for _ in range(40):                                  # occluding near / far rectangles
+        b, v, u = rng.integers(0, 2), rng.integers(0, 440), rng.integers(0, 600)
+        h, w = rng.integers(3, 40), rng.integers(3, 40)
+        z[b, v:v + h, u:u + w] *= rng.choice([0.01, 100.0])
+    z = z.astype(np.float32)
+    for K in (ts.Intrinsics(500.0, 470.0, 321.3, 238.9), ts.Intrinsics(5.0, 5.0, 320.0, 240.0),
+              ts.Intrinsics(5e4, 4.5e4, -100.0, 900.0)):
+        for f in ("fd", "sobel"):
+            for m in MODES:
+                g, _ = check(tfn, z, K, f, m)
+                for kernel in ("general", "pixel"):
+                    gk = run_gpu(tfn, z, K, f, m, kernel=kernel)
+                    assert np.array_equal(g.view(np.uint32), gk.view(np.uint32)), (scale, K, f, m, kernel)
