@@ -552,3 +552,25 @@ def test_extreme_depth_scales_and_occlusions(tfn, random8, scale):
                 for kernel in ("general", "pixel"):
                     gk = run_gpu(tfn, z, K, f, m, kernel=kernel)
                     assert np.array_equal(g.view(np.uint32), gk.view(np.uint32)), (scale, K, f, m, kernel)
+
+
+@pytest.mark.parametrize("scale", [1e-3, 1.0, 1e3])
+def test_extreme_disparity_and_noise(tfn, random8, scale):
+    """disparity maps scaled over six decades with 100x occlusion steps, and every filter on
+    heavily noisy depth (S:374 high preset): parity and bit-identical kernels"""
+    d = ts.depth_to_disparity(random8.depth64[:2], 500.0, 0.12).numpy().astype(np.float64) * scale
+    rng = np.random.default_rng(int(scale * 7) + 1)
+    for _ in range(40):
+        b, v, u = rng.integers(0, 2), rng.integers(0, 440), rng.integers(0, 600)
+        d[b, v:v + rng.integers(3, 40), u:u + rng.integers(3, 40)] *= rng.choice([0.01, 100.0])
+    d = d.astype(np.float32)
+    for f in ("fd", "scharr"):
+        for m in MODES:
+            g, _ = check(tfn, d, ts.K_VGA, f, m, disp=True)
+            gk = run_gpu(tfn, d, ts.K_VGA, f, m, disp=True, kernel="general")
+            assert np.array_equal(g.view(np.uint32), gk.view(np.uint32)), (scale, f, m)
+    if scale == 1.0:
+        z = ts.add_gaussian_noise(random8.depth[:2], ts.NOISE_PRESETS["high"], seed=5).numpy()
+        for f in FILTERS:
+            for m in MODES:
+                check(tfn, z, ts.K_VGA, f, m)
