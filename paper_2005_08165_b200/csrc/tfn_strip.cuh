@@ -105,7 +105,6 @@ __device__ __forceinline__ void load_raw(Slot& s, const StripCtx<unsigned short>
 // Q5 for the fast path: valid iff finite and >= FLT_MIN (rejects 0, negatives, NaN,
 // +-Inf, subnormals).  An invalid sample becomes NaN, which makes every candidate that
 // uses it NaN and so sends the pixel to the exact path.
-template <bool DISP>
 __device__ __forceinline__ float sanitize_fast(float z, bool ok) {
     const bool good = valid_bits(z) & ok;      // no short circuit: FSEL, not a branch
     return good ? z : __int_as_float(0x7fffffff);
@@ -113,10 +112,10 @@ __device__ __forceinline__ float sanitize_fast(float z, bool ok) {
 
 template <bool DISP, bool GEN, class T>
 __device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
-    s.z[0] = sanitize_fast<DISP>(s.raw[0], s.rok && c.okl);
+    s.z[0] = sanitize_fast(s.raw[0], s.rok && c.okl);
 #pragma unroll
-    for (int j = 1; j <= PPL; ++j) s.z[j] = sanitize_fast<DISP>(s.raw[j], s.rok && c.okm);
-    s.z[PPL + 1] = sanitize_fast<DISP>(s.raw[PPL + 1], s.rok && c.okr);
+    for (int j = 1; j <= PPL; ++j) s.z[j] = sanitize_fast(s.raw[j], s.rok && c.okm);
+    s.z[PPL + 1] = sanitize_fast(s.raw[PPL + 1], s.rok && c.okr);
     // exact for every valid sample; invalid ones give finite garbage here, but their
     // NaN z makes the pixel "special", which recomputes it exactly
 #pragma unroll
@@ -220,7 +219,7 @@ __device__ __forceinline__ void store_packed(__half* o, const float* x, const fl
 // computed here).
 template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
-                                         char* __restrict__ out, long long HW, int layout,
+                                         char* __restrict__ out, long long HW,
                                          unsigned colmask, float vf) {
     load_raw(C, c, v + 3);                       // prefetch three rows ahead (C.raw is free)
     prepare<DISP, GEN>(N, c);
@@ -445,7 +444,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
 
 // Rows [ys, y1) of one strip: prologue, then the rolling window down the strip.
 template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT>
-__device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long long HW, int layout,
+__device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long long HW,
                                           unsigned colmask, int ys, int y1) {
     Slot S0, S1, S2;
     // prologue: rows ys-1 (S0), ys (S1) prepared; row ys+1 (S2) loaded
@@ -466,11 +465,11 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
     }
     float vf = __int2float_rn(ys);      // exact row index as float (rows < 2^24)
     for (int v = ys; v < y1; v += 3) {
-        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S0, S1, S2, v, c, out, HW, layout, colmask, vf);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S0, S1, S2, v, c, out, HW, colmask, vf);
         if (v + 1 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S1, S2, S0, v + 1, c, out, HW, layout, colmask, vf + 1.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S1, S2, S0, v + 1, c, out, HW, colmask, vf + 1.0f);
         if (v + 2 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S2, S0, S1, v + 2, c, out, HW, layout, colmask, vf + 2.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S2, S0, S1, v + 2, c, out, HW, colmask, vf + 2.0f);
         vf += 3.0f;
     }
 }
@@ -532,7 +531,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
         char* out = reinterpret_cast<char*>(p.out) + cb * (fb * nc * HW + (LAYOUT == 0 ? (long long)c.cm : (long long)nc * c.cm));
         c.pts = p.pts ? p.pts + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm) : nullptr;
 
-        strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS, OUT>(c, out, HW, p.layout, colmask, y0, y1);
+        strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS, OUT>(c, out, HW, colmask, y0, y1);
         if (p.work) {
             int nxt = 0;
             if (lane == 0) nxt = atomicAdd(p.work, 1);
