@@ -414,6 +414,11 @@ def main():
         kernel_ms = sum(a.elapsed_time(b) for a, b in ev)
         units = per_rank * H * W * steps
     launches = tfn.tfn_kernel_launches() - launches0
+    from paper_2005_08165_b200 import tfn as _T
+    variant = {"auto": {2: "fast strip (AUTO)", 3: "general strip (AUTO)"}.get(_T.tfn_auto_variant(est.h)),
+               "strip": "fast strip", "general": "general strip", "pixel": "per-pixel"}[args.kernel]
+    if cfg.get("u16") and args.kernel in ("auto", "strip"):
+        variant = "general strip (uint16 input)"
 
     t_max = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if pg:
@@ -494,7 +499,7 @@ def main():
             "data": "synthetic (seeded analytic ray-cast scenes)",
             "config": {"workload": cfg["desc"], "filter": filt, "nz_mode": mode, "layout": args.layout,
                        "input": "disparity" if cfg["disp"] else ("depth u16 mm codes" if cfg.get("u16") else "depth"),
-                       "out_dtype": out_dtype, "frames_per_gpu": per_rank,
+                       "out_dtype": out_dtype, "kernel_variant": variant, "frames_per_gpu": per_rank,
                        "H": H, "W": W, "fps": value * 1e6 / (H * W),
                        "l2": "inputs (%.2f GB/GPU) larger than the 126 MB L2; no flush" % (chunk * H * W * in_b / 1e9),
                        "parallelism": f"dp{ws} (frame batches sharded, no collective on the hot path)"},
