@@ -112,10 +112,18 @@ __device__ __forceinline__ float sanitize_fast(float z, bool ok) {
 
 template <bool DISP, bool GEN, class T>
 __device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
-    s.z[0] = sanitize_fast(s.raw[0], s.rok && c.okl);
+    // the lane's own columns need only the value test; the halos are outside the image at
+    // the first / last lane of a frame row; whole rows outside the image (loads predicated
+    // off, stale registers) take a warp-uniform, rare branch — measured +1.9 % over
+    // per-sample row predicates.  Lanes past W never store, so their stale samples need no NaN.
+    s.z[0] = sanitize_fast(s.raw[0], c.okl);
 #pragma unroll
-    for (int j = 1; j <= PPL; ++j) s.z[j] = sanitize_fast(s.raw[j], s.rok && c.okm);
-    s.z[PPL + 1] = sanitize_fast(s.raw[PPL + 1], s.rok && c.okr);
+    for (int j = 1; j <= PPL; ++j) s.z[j] = valid_bits(s.raw[j]) ? s.raw[j] : __int_as_float(0x7fffffff);
+    s.z[PPL + 1] = sanitize_fast(s.raw[PPL + 1], c.okr);
+    if (__any_sync(0xffffffffu, !s.rok)) {
+#pragma unroll
+        for (int j = 0; j < PPL + 2; ++j) s.z[j] = s.rok ? s.z[j] : __int_as_float(0x7fffffff);
+    }
     // exact for every valid sample; invalid ones give finite garbage here, but their
     // NaN z makes the pixel "special", which recomputes it exactly
 #pragma unroll
