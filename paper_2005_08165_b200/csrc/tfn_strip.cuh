@@ -354,6 +354,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         float2 phi;
         if (MODE == MEAN) {
             phi = __fmul2_rn(sum8, f2(0.125f, 0.125f));
+            phi = __ffma2_rn(f2(0.f, 0.f), sum8, phi);        // +-inf sum -> NaN Phi (special)
         } else {
             float t0[8], t1[8];
 #pragma unroll
@@ -381,8 +382,10 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         // special: a non-finite candidate or Phi == 0 at a pixel whose centre is valid (an
         // invalid centre poisons every candidate through m~ = m * NaN: the fast path
         // already wrote the canonical NaN)
-        const bool sp0 = (!(fabsf(sum8.x) < __int_as_float(0x7f800000)) || (phi.x == 0.f)) && !isnan(zc2.x);
-        const bool sp1 = (!(fabsf(sum8.y) < __int_as_float(0x7f800000)) || (phi.y == 0.f)) && !isnan(zc2.y);
+        // Phi is NaN iff a candidate is non-finite (the median's fold above, the mean's fold
+        // below), so one compare per pixel covers "non-finite candidate or Phi == 0"
+        const bool sp0 = !(fabsf(phi.x) > 0.f) && !isnan(zc2.x);
+        const bool sp1 = !(fabsf(phi.y) > 0.f) && !isnan(zc2.y);
         special |= (sp0 ? (1u << i0) : 0u) | (sp1 ? (1u << i1) : 0u);
     }
 
