@@ -381,9 +381,8 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         nx[i0] = ox.x; nx[i1] = ox.y; ny[i0] = oy.x; ny[i1] = oy.y; nz[i0] = oz.x; nz[i1] = oz.y;
         // special: a non-finite candidate or Phi == 0 at a pixel whose centre is valid (an
         // invalid centre poisons every candidate through m~ = m * NaN: the fast path
-        // already wrote the canonical NaN)
-        // Phi is NaN iff a candidate is non-finite (the median's fold above, the mean's fold
-        // below), so one compare per pixel covers "non-finite candidate or Phi == 0"
+        // already wrote the canonical NaN).  Phi is NaN iff a candidate is non-finite (the
+        // folds above), so one compare per pixel covers both.
         const bool sp0 = !(fabsf(phi.x) > 0.f) && !isnan(zc2.x);
         const bool sp1 = !(fabsf(phi.y) > 0.f) && !isnan(zc2.y);
         special |= (sp0 ? (1u << i0) : 0u) | (sp1 ? (1u << i1) : 0u);
