@@ -4,10 +4,12 @@
 // Geometry.  One warp owns a strip of 32*PPL columns (PPL = 4: 128) x strip_h rows of one
 // frame; each lane owns PPL adjacent columns and walks down the strip with a rolling
 // window of three row "slots" (rows v-1, v, v+1).  The row loop is unrolled by 3 and the
-// slots rotate by renaming (no register copies).  Per lane-row: one LDG.128 (fp32) or
-// LDG.64 (uint16) + two predicated halo loads in, three STG.128 (fp32) / STG.64 (half) /
-// one or two vector stores (oct16) out, loads prefetched three rows ahead.  Persistent
-// grid; strips handed out by an atomic work counter (dynamic scheduling).
+// slots rotate by renaming (no register copies).  Per lane-row: fp32 input one LDG.128 +
+// two predicated halo loads, prefetched three rows ahead into registers; uint16 input one
+// cp.async of 8 B into a per-warp shared-memory ring TFN_CPA_D rows ahead (halo words by
+// the edge lanes), read back with LDS; out: three STG.128 (fp32) / STG.64 (half) / one or
+// two vector stores (oct16).  Persistent grid; strips handed out by an atomic work counter
+// (dynamic scheduling).
 //
 // Arithmetic (bit-identical to tfn_pixel_kernel, see tfn_device.cuh):
 //   fp64:  w = 1/z (faithful, ~2^-66), D_h, D_v, g_u, g_v in the oracle's order,
@@ -27,6 +29,12 @@
 //                invalid resolved by finish_tail: the per-pixel kernel's code, inline.
 #pragma once
 
+#ifndef TFN_U16_MINBLOCKS
+#define TFN_U16_MINBLOCKS 4      // resident CTAs per SM of the uint16 (ring) instantiations (128 registers: +2.3 % over 3)
+#endif
+#ifndef TFN_CPA_D
+#define TFN_CPA_D 6              // cp.async ring prefetch distance (rows), <= 8
+#endif
 #ifndef TFN_STRIP_PPL
 #define TFN_STRIP_PPL 4          // pixels (columns) per lane: 4 or 2
 #endif
@@ -62,12 +70,66 @@ struct StripCtx {
     float pscale, ifx, ify;   // Z = pscale * sample (depth) or pscale / d (disparity); 1/fx, 1/fy
     Wts wt;            // CUSTOM filter weights
     float v0;
+    int y1;            // end row of the current strip
+    unsigned ring;     // shared-memory address of this warp's row ring (uint16 input)
+    int lane;
 };
+
+
 
 // uint16 code -> float, exactly, without a conversion instruction: 2^23 + code has the code
 // in its low mantissa bits (PRMT builds the word, one FADD removes the 2^23)
 __device__ __forceinline__ float code_lo(unsigned x) { return __uint_as_float(__byte_perm(x, 0x4B00u, 0x5410)) - 8388608.0f; }
 __device__ __forceinline__ float code_hi(unsigned x) { return __uint_as_float(__byte_perm(x, 0x4B00u, 0x5432)) - 8388608.0f; }
+
+// Row staging.  fp32 input: register window, LDG three rows ahead (load_raw).  uint16 input
+// (N1): a per-warp shared-memory ring filled by cp.async TFN_CPA_D rows ahead — measured
+// +20 % on uint16 codes -> half normals (158.8 vs 132.0 Gpx/s), but -5 % on the fp32 fast
+// variant and -2 % on the fp32 general one, so fp32 keeps the register window.
+template <class T> struct Ring { static constexpr bool on = sizeof(T) == 2; };
+// The ring: 8 rows per warp, RB bytes per row: [12 B pad | left halo word | the
+// strip's 32*PPL samples | right halo word | pad]; lane l's vector at byte 16 + l*PPL*sizeof(T)
+constexpr int RING_RB = 16 + 32 * 4 * 4 + 16;
+
+__device__ __forceinline__ void cpa(unsigned dst, const void* src, int bytes_ok, int size) {
+    if (size == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(src), "r"(bytes_ok) : "memory");
+    else if (size == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" :: "r"(dst), "l"(src), "r"(bytes_ok) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" :: "r"(dst), "l"(src), "r"(bytes_ok) : "memory");
+}
+__device__ __forceinline__ unsigned ring_base() {
+    __shared__ __align__(16) char ring[TFN_STRIP_THREADS / 32][8][RING_RB];
+    return (unsigned)__cvta_generic_to_shared(&ring[threadIdx.x >> 5][0][0]);
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" :: "n"(N) : "memory"); }
+
+// issue row v of the strip into its ring slot; rows outside the image, halos outside the
+// image and lanes past W are zero-filled (0 is an invalid sample: Q5), so the sanitize needs
+// no position predicates
+template <class T>
+__device__ __forceinline__ void issue_row(const StripCtx<T>& c, int v) {
+    const bool rin = (v >= 0) && (v < c.H);
+    const unsigned slot = c.ring + ((v + 1) & 7) * RING_RB;
+    const T* row = c.pm + (rin ? v : 0) * c.W;
+    constexpr int VB = PPL * sizeof(T);
+    cpa(slot + 16 + c.lane * VB, row, (rin && c.okm) ? VB : 0, VB);
+    // halo words: fp32 the sample itself; uint16 the aligned pair holding it
+    // (zero-filled halos keep an in-image source address: nothing is read from it)
+    if (c.lane == 0) cpa(slot + 12, reinterpret_cast<const char*>(row) - (c.okl ? 4 : 0), (rin && c.okl) ? 4 : 0, 4);
+    if (c.lane == 31) cpa(slot + 16 + 32 * VB, row + (c.okr ? PPL : 0), (rin && c.okr) ? 4 : 0, 4);
+}
+__device__ __forceinline__ void fetch_row(Slot& s, const StripCtx<unsigned short>& c, int v) {
+    const char* slot = reinterpret_cast<const char*>(__cvta_shared_to_generic(c.ring + ((v + 1) & 7) * RING_RB));
+    const char* me = slot + 16 + c.lane * 8;
+    const uint2 m = *reinterpret_cast<const uint2*>(me);
+    s.raw[1] = code_lo(m.x); s.raw[2] = code_hi(m.x); s.raw[3] = code_lo(m.y); s.raw[4] = code_hi(m.y);
+    s.raw[0] = code_hi(*reinterpret_cast<const unsigned*>(me - 4));
+    s.raw[5] = code_lo(*reinterpret_cast<const unsigned*>(me + 8));
+    s.rok = true;
+}
 
 // row v of the lane's window: one LDG.128 (fp32) or LDG.64 (uint16) + two halo loads at
 // immediate offsets, predicated off outside the image (never an out-of-bounds address)
@@ -116,11 +178,11 @@ __device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
     // the first / last lane of a frame row; whole rows outside the image (loads predicated
     // off, stale registers) take a warp-uniform, rare branch — measured +1.9 % over
     // per-sample row predicates.  Lanes past W never store, so their stale samples need no NaN.
-    s.z[0] = sanitize_fast(s.raw[0], c.okl);
+    s.z[0] = sanitize_fast(s.raw[0], Ring<T>::on || c.okl);
 #pragma unroll
     for (int j = 1; j <= PPL; ++j) s.z[j] = valid_bits(s.raw[j]) ? s.raw[j] : __int_as_float(0x7fffffff);
-    s.z[PPL + 1] = sanitize_fast(s.raw[PPL + 1], c.okr);
-    if (__any_sync(0xffffffffu, !s.rok)) {
+    s.z[PPL + 1] = sanitize_fast(s.raw[PPL + 1], Ring<T>::on || c.okr);
+    if (!Ring<T>::on && __any_sync(0xffffffffu, !s.rok)) {
 #pragma unroll
         for (int j = 0; j < PPL + 2; ++j) s.z[j] = s.rok ? s.z[j] : __int_as_float(0x7fffffff);
     }
@@ -229,7 +291,16 @@ template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, i
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
                                          char* __restrict__ out, long long HW,
                                          unsigned colmask, float vf) {
-    load_raw(C, c, v + 3);                       // prefetch three rows ahead (C.raw is free)
+    if constexpr (Ring<T>::on) {
+        // ring: rows up to v+D-1 in flight; row v+1 is complete once at most D-2 groups are pending
+        if (v + TFN_CPA_D - 1 <= c.y1) issue_row(c, v + TFN_CPA_D - 1);
+        cpa_commit();
+        cpa_wait<TFN_CPA_D - 2>();
+        __syncwarp();                                // halo words come from the neighbour lanes' copies
+        fetch_row(N, c, v + 1);
+    } else {
+        load_raw(C, c, v + 3);                       // prefetch three rows ahead (C.raw is free)
+    }
     prepare<DISP, GEN>(N, c);
 
     // ---- fp64 gradients (Eq. 15), oracle order (Q10) ----
@@ -457,13 +528,28 @@ template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, i
 __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long long HW,
                                           unsigned colmask, int ys, int y1) {
     Slot S0, S1, S2;
-    // prologue: rows ys-1 (S0), ys (S1) prepared; row ys+1 (S2) loaded
-    load_raw(S0, c, ys - 1);
-    load_raw(S1, c, ys);
-    load_raw(S2, c, ys + 1);
-    prepare<DISP, GEN>(S0, c);
-    prepare<DISP, GEN>(S1, c);
-    load_raw(S0, c, ys + 2);
+    if constexpr (Ring<T>::on) {
+        // prologue: rows ys-1 .. ys+D-2 issued (one group each), rows ys-1 (S0), ys (S1) prepared
+    #pragma unroll
+        for (int r = -1; r <= TFN_CPA_D - 2; ++r) {
+            if (ys + r <= y1) issue_row(c, ys + r);
+            cpa_commit();
+        }
+        cpa_wait<TFN_CPA_D - 2>();
+        __syncwarp();
+        fetch_row(S0, c, ys - 1);
+        fetch_row(S1, c, ys);
+        prepare<DISP, GEN>(S0, c);
+        prepare<DISP, GEN>(S1, c);
+    } else {
+        // prologue: rows ys-1 (S0), ys (S1) prepared; row ys+1 (S2) loaded
+        load_raw(S0, c, ys - 1);
+        load_raw(S1, c, ys);
+        load_raw(S2, c, ys + 1);
+        prepare<DISP, GEN>(S0, c);
+        prepare<DISP, GEN>(S1, c);
+        load_raw(S0, c, ys + 2);
+    }
 #pragma unroll
     for (int i = 0; i < PPL; ++i) {
         S1.head[i] = grad_head<F>(Taps<F>::corners ? __dsub_rn(S0.w[i + 2], S0.w[i]) : 0.0,
@@ -493,7 +579,7 @@ template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS, int
 #ifdef TFN_STRIP_MAXNREG
 __global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(KernelArgs p) {
 #else
-__global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_strip_kernel(KernelArgs p) {
+__global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T>::on ? TFN_U16_MINBLOCKS : TFN_STRIP_MINBLOCKS) tfn_strip_kernel(KernelArgs p) {
 #endif
     const int lane = threadIdx.x & 31;
     const int warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -510,6 +596,8 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
     c.fired = p.fired;
     c.wt.kp = p.kp; c.wt.k0 = p.k0;
     c.outk = (OUT == 2) ? p.out_kind : (OUT == 3 ? 2 : OUT);
+    c.lane = lane;
+    if constexpr (Ring<T>::on) c.ring = ring_base();
     c.pscale = p.pscale; c.ifx = p.ifx; c.ify = p.ify;
     const int cb = c.outk == 0 ? 4 : 2;          // bytes per stored component
     const int nc = c.outk == 2 ? 2 : 3;          // stored components per pixel
@@ -541,6 +629,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, TFN_STRIP_MINBLOCKS) tfn_st
         char* out = reinterpret_cast<char*>(p.out) + cb * (fb * nc * HW + (LAYOUT == 0 ? (long long)c.cm : (long long)nc * c.cm));
         c.pts = p.pts ? p.pts + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm) : nullptr;
 
+        c.y1 = y1;
         strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS, OUT>(c, out, HW, colmask, y0, y1);
         if (p.work) {
             int nxt = 0;
