@@ -85,8 +85,9 @@ __device__ __forceinline__ float code_hi(unsigned x) { return __uint_as_float(__
 // Row staging.  fp32 input: register window, LDG three rows ahead (load_raw).  uint16 input
 // (N1): a per-warp shared-memory ring filled by cp.async TFN_CPA_D rows ahead — measured
 // +20 % on uint16 codes -> half normals (158.8 vs 132.0 Gpx/s), but -5 % on the fp32 fast
-// variant and -2 % on the fp32 general one, so fp32 keeps the register window.
-template <class T> struct Ring { static constexpr bool on = sizeof(T) == 2; };
+// variant and +-0.5 % on the fp32 general one, so fp32 keeps the register window (and 3
+// CTAs/SM: 4 with 128 registers runs the general variant 8 % slower).
+template <class T, bool GEN> struct Ring { static constexpr bool on = sizeof(T) == 2; };
 // The ring: 8 rows per warp, RB bytes per row: [12 B pad | left halo word | the
 // strip's 32*PPL samples | right halo word | pad]; lane l's vector at byte 16 + l*PPL*sizeof(T)
 constexpr int RING_RB = 16 + 32 * 4 * 4 + 16;
@@ -178,11 +179,11 @@ __device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
     // the first / last lane of a frame row; whole rows outside the image (loads predicated
     // off, stale registers) take a warp-uniform, rare branch — measured +1.9 % over
     // per-sample row predicates.  Lanes past W never store, so their stale samples need no NaN.
-    s.z[0] = sanitize_fast(s.raw[0], Ring<T>::on || c.okl);
+    s.z[0] = sanitize_fast(s.raw[0], Ring<T, GEN>::on || c.okl);
 #pragma unroll
     for (int j = 1; j <= PPL; ++j) s.z[j] = valid_bits(s.raw[j]) ? s.raw[j] : __int_as_float(0x7fffffff);
-    s.z[PPL + 1] = sanitize_fast(s.raw[PPL + 1], Ring<T>::on || c.okr);
-    if (!Ring<T>::on && __any_sync(0xffffffffu, !s.rok)) {
+    s.z[PPL + 1] = sanitize_fast(s.raw[PPL + 1], Ring<T, GEN>::on || c.okr);
+    if (!Ring<T, GEN>::on && __any_sync(0xffffffffu, !s.rok)) {
 #pragma unroll
         for (int j = 0; j < PPL + 2; ++j) s.z[j] = s.rok ? s.z[j] : __int_as_float(0x7fffffff);
     }
@@ -291,7 +292,7 @@ template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, i
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
                                          char* __restrict__ out, long long HW,
                                          unsigned colmask, float vf) {
-    if constexpr (Ring<T>::on) {
+    if constexpr (Ring<T, GEN>::on) {
         // ring: rows up to v+D-1 in flight; row v+1 is complete once at most D-2 groups are pending
         if (v + TFN_CPA_D - 1 <= c.y1) issue_row(c, v + TFN_CPA_D - 1);
         cpa_commit();
@@ -528,7 +529,7 @@ template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, i
 __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long long HW,
                                           unsigned colmask, int ys, int y1) {
     Slot S0, S1, S2;
-    if constexpr (Ring<T>::on) {
+    if constexpr (Ring<T, GEN>::on) {
         // prologue: rows ys-1 .. ys+D-2 issued (one group each), rows ys-1 (S0), ys (S1) prepared
     #pragma unroll
         for (int r = -1; r <= TFN_CPA_D - 2; ++r) {
@@ -579,7 +580,7 @@ template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS, int
 #ifdef TFN_STRIP_MAXNREG
 __global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(KernelArgs p) {
 #else
-__global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T>::on ? TFN_U16_MINBLOCKS : TFN_STRIP_MINBLOCKS) tfn_strip_kernel(KernelArgs p) {
+__global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T, KV == 1>::on ? TFN_U16_MINBLOCKS : TFN_STRIP_MINBLOCKS) tfn_strip_kernel(KernelArgs p) {
 #endif
     const int lane = threadIdx.x & 31;
     const int warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -597,7 +598,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T>::on ? TFN_U16_MINBL
     c.wt.kp = p.kp; c.wt.k0 = p.k0;
     c.outk = (OUT == 2) ? p.out_kind : (OUT == 3 ? 2 : OUT);
     c.lane = lane;
-    if constexpr (Ring<T>::on) c.ring = ring_base();
+    if constexpr (Ring<T, KV == 1>::on) c.ring = ring_base();
     c.pscale = p.pscale; c.ifx = p.ifx; c.ify = p.ify;
     const int cb = c.outk == 0 ? 4 : 2;          // bytes per stored component
     const int nc = c.outk == 2 ? 2 : 3;          // stored components per pixel
