@@ -17,7 +17,7 @@ python bench.py --config 3 --mode mean --filter fd --steps 20 --warmup 3 --no-cp
 python bench.py --mode mean --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_cfg2_mean_${TAG}.log 2>&1
 python bench.py --layout packed --steps 20 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_cfg2_packed_${TAG}.log 2>&1
 CMD="python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e"
-$CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
+[ -z "$NO_NCU" ] && $CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:tfn_ --csv \
     --log-file gpurun_out/launches_default_${TAG}.csv $CMD > gpurun_out/ncu_launch_default_${TAG}.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:tfn_strip -s 4 -c 1 \
