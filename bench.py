@@ -350,7 +350,8 @@ def main():
         torch.cuda.synchronize()
     step = lambda: launch(x, out)            # noqa: E731
     if use_graph:
-        # launch-bound single frames: the step's launch (work-counter memset + kernel) is
+        # launch-bound single frames: the step's launch (the kernel; a work-counter memset
+        # only when the batch has more strips than the grid has warps) is
         # captured once into a CUDA graph and replayed, so host launch overhead is off the
         # device timeline; the kernel and its arguments are the same as a direct call
         g = torch.cuda.CUDAGraph()

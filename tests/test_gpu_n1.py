@@ -174,3 +174,22 @@ def test_oct16_normals(tfn):
     oku = np.all(np.isfinite(ru), 1)
     assert np.array_equal(oku, np.all(np.isfinite(nu), 1))
     assert metrics.angular_error_deg(np.moveaxis(nu, 1, -1)[oku], np.moveaxis(ru, 1, -1)[oku]).max() < 0.005
+
+
+@pytest.mark.parametrize("H,W", [(3, 4), (5, 8), (37, 132), (64, 260), (50, 644), (130, 388)])
+def test_u16_ring_ragged_bitwise(tfn, H, W):
+    """the uint16 strip kernels stage rows through a cp.async shared-memory ring whose
+    out-of-image rows, halos and lanes past W are zero-filled (code 0 = invalid): on ragged
+    shapes (W % 128 != 0, tiny H) and odd strip heights they still equal the fp32 per-pixel
+    kernel on (float)code bit for bit, both layouts, both strip variants"""
+    codes = mm_codes(frames=2, seed=40 + H, H=H, W=W, K=ts.Intrinsics(W * 0.8, W * 0.8, W / 2 - 0.5, H / 2 - 0.5),
+                     holes=True)
+    K = ts.Intrinsics(W * 0.8, W * 0.8, W / 2 - 0.5, H / 2 - 0.5)
+    zf = codes.astype(np.float32)
+    for f, m in (("sobel", "median"), ("fd", "mean"), ("scharr", "mean")):
+        ref = run_f32(tfn, zf, K, f, m, kernel="pixel")
+        for kernel in ("strip", "general"):
+            for sh in (0, 7, 13):
+                assert same_bits(run_u16(tfn, codes, K, f, m, kernel=kernel, strip_h=sh), ref), (f, m, kernel, sh)
+        pk = run_u16(tfn, codes, K, f, m, layout="packed", strip_h=5)
+        assert same_bits(pk.permute(0, 3, 1, 2).contiguous(), ref), (f, m, "packed")
