@@ -408,19 +408,23 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         }
         if (GEN) {
             // general variant: skipped candidates, flat, ties and invalid pixels handled in
-            // registers by the same code as the per-pixel kernel (bit-identical results)
+            // registers by the same arithmetic as the per-pixel kernel (bit-identical results)
+            float ph[2];
+            bool none[2], okc[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int i = 2 * q + h;
                 float t[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) t[k] = h ? tau[k].y : tau[k].x;
                 int kk;
-                const float ph = phi_any<MODE>(t, h ? sum8.y : sum8.x, kk);
-                const Normal n = finish_tail(!isnan(C.z[i + 1]), gu32[i], gv32[i], ph, kk == 0, c.a[i], b,
-                                             c.fx, c.fy);
-                nx[i] = n.x; ny[i] = n.y; nz[i] = n.z;
+                ph[h] = phi_any<MODE>(t, h ? sum8.y : sum8.x, kk);
+                none[h] = kk == 0;
+                okc[h] = !isnan(C.z[2 * q + h + 1]);
             }
+            Normal n0, n1;
+            finish_tail2(okc, mu, mv, f2(ph[0], ph[1]), none, f2(c.a[i0], c.a[i1]), b, c.fx, c.fy, n0, n1);
+            nx[i0] = n0.x; ny[i0] = n0.y; nz[i0] = n0.z;
+            nx[i1] = n1.x; ny[i1] = n1.y; nz[i1] = n1.z;
             continue;
         }
         float2 phi;
