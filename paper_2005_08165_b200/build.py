@@ -41,7 +41,8 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     for src in SOURCES:
         tag = os.path.basename(SO_).replace(".so", "")
         obj = os.path.join(HERE, "build", f"{tag}_{src.replace('.cu', '.o')}")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
+        extra = os.environ.get("TFN_NVCC_EXTRA", "").split()      # A/B of compiler knobs (tools/build_ab.py)
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)
