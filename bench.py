@@ -72,7 +72,7 @@ def parse():
     ap.add_argument("--layout", default="planar", choices=["planar", "packed"])
     ap.add_argument("--out", default=None, choices=["f32", "f16", "oct16"], help="normal encoding (default: the config's)")
     ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel", "general"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel", "general", "masked"])
     ap.add_argument("--strip-h", type=int, default=0)
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--static", action="store_true", help="static strip scheduling")
@@ -416,8 +416,10 @@ def main():
         units = per_rank * H * W * steps
     launches = tfn.tfn_kernel_launches() - launches0
     from paper_2005_08165_b200 import tfn as _T
-    variant = {"auto": {2: "fast strip (AUTO)", 3: "general strip (AUTO)"}.get(_T.tfn_auto_variant(est.h)),
-               "strip": "fast strip", "general": "general strip", "pixel": "per-pixel"}[args.kernel]
+    variant = {"auto": {2: "fast strip (AUTO)", 3: "general strip (AUTO)", 4: "masked strip (AUTO)"}.get(
+                   _T.tfn_auto_variant(est.h)),
+               "strip": "fast strip", "general": "general strip", "masked": "masked strip",
+               "pixel": "per-pixel"}[args.kernel]
     if cfg.get("u16") and args.kernel in ("auto", "strip"):
         variant = "general strip (uint16 input)"
 

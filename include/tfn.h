@@ -75,7 +75,9 @@ typedef enum { TFN_OUT_F32 = 0, TFN_OUT_F16 = 1, TFN_OUT_OCT16 = 2 } tfn_out_dty
 /* Options for tfn_set_option (tuning / testing; defaults are the production path) */
 typedef enum {
     TFN_OPT_KERNEL = 0,     /* 0 auto, 1 per-pixel kernel, 2 strip kernel (needs W%4==0, 16-B alignment),  */
-                            /* 3 general strip kernel (same results; no special path: for holes / quantized)  */
+                            /* 3 general strip kernel (same results; no special path: for holes / quantized), */
+                            /* 4 masked strip kernel (same results; special path only for pixels whose taps  */
+                            /*   are all valid: for depth with holes / dropout)                               */
     TFN_OPT_STRIP_H = 1,    /* rows per warp strip, 0 = auto (>= 4)                                        */
     TFN_OPT_GRID = 2,       /* CTAs of the strip kernel, 0 = auto (resident CTAs x SMs)                    */
     TFN_OPT_DYNAMIC = 3,    /* 1 (default): strips claimed from a per-call work counter; 0: static stride  */
@@ -201,12 +203,15 @@ const char* tfn_status_string(int status);
 unsigned long long tfn_kernel_launches(void);
 
 /* The strip variant TFN_OPT_KERNEL = 0 (AUTO) currently picks for handle h: *variant = 2
- * (fast strip kernel + exact per-pixel special path) or 3 (general strip kernel).  AUTO
- * starts fast; the fast kernel counts the row steps that needed its special path, the count
- * returns asynchronously (pinned word + event, read at a later call, never a sync), and
- * above 20 % of row steps AUTO switches to the general kernel (below 10 % back; general
- * mode re-probes with the fast kernel every 32nd call).  Results are bit-identical either
- * way; only speed differs.  Returns TFN_ERR_INVALID_ARGUMENT for NULLs. */
+ * (fast strip kernel + exact per-pixel special path), 4 (masked: the fast kernel whose
+ * special path skips pixels with an invalid tap — their NaN is already exact) or 3 (general
+ * strip kernel).  AUTO starts fast; the fast and masked kernels count the row steps that
+ * needed their special path, the count returns asynchronously (pinned word + event, read at
+ * a later call, never a sync), and above 20 % of row steps AUTO steps fast -> masked ->
+ * general (below 10 % back; masked / general mode re-probe the variant below every 32nd
+ * call).  Results are bit-identical either way; only speed differs.
+ * uint16 input and the point cloud always run the general kernel.  Returns
+ * TFN_ERR_INVALID_ARGUMENT for NULLs. */
 int tfn_auto_variant(tfn_handle h, int* variant);
 
 /* ABI version (major*10000 + minor*100 + patch). */

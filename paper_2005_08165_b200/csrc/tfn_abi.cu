@@ -43,30 +43,34 @@ struct tfn_ctx {
     int dynamic = 1;
     int device = 0;
     int sms = 148;
-    int strip_ctas_per_sm[2][2] = {{0, 0}, {0, 0}};   // fp32 input: [fast, general][depth, disparity]
+    int strip_ctas_per_sm[3][2] = {{0, 0}, {0, 0}, {0, 0}};   // fp32 input: [fast, general, masked][depth, disparity]
     int strip_ctas_u16 = 0;                           // uint16 depth codes (general variant)
     std::mutex ws_mu;
     Workspace ws;
     int* work = nullptr;                 // ring of per-call {work, fired} counter pairs
     std::atomic<unsigned> call_seq{0};
-    // AUTO kernel selection: the fast strip variant counts its special row steps; the count
-    // comes back through a pinned word a few calls later and picks fast vs general
+    // AUTO kernel selection: the fast and masked strip variants count their special row
+    // steps; the count comes back through a pinned word a few calls later and moves the
+    // choice fast -> masked -> general (and back)
     std::mutex auto_mu;
     int* fb_host = nullptr;              // pinned: fired row steps of the last probed launch
     cudaEvent_t fb_ev = nullptr;
     bool fb_pending = false;
     double fb_steps = 0;                 // row steps of that launch
-    int auto_general = 0;                // current AUTO choice: 0 fast, 1 general
+    int auto_state = 0;                  // current AUTO choice: 0 fast, 1 masked, 2 general
+    int fb_variant = 0;                  // variant of the pending probe: 0 fast, 1 masked
     unsigned auto_calls = 0;
 };
 #define TFN_WORK_RING 4096
-// AUTO: general variant when more than this fraction of the fast variant's row steps needed
-// the special path (measured break-even ~0.24: config 2 has 0.011 and runs 210 vs 160 Gpx/s
-// fast vs general; config 4 (holes + 1 % salt) has 0.98 and runs 92.5 vs 157)
+// AUTO: step to the next variant (fast -> masked -> general) when more than this fraction
+// of the probed variant's row steps needed the special path (measured break-even ~0.24:
+// config 2 has 0.011 and runs 217 fast vs 189 masked vs 167 general; config 4 (holes + 1 %
+// salt) fires on 0.98 of the fast variant's row steps but few of the masked one's, and
+// runs 94 fast vs 175 masked vs 164 general); back below TFN_AUTO_FAST_BELOW
 #define TFN_AUTO_GENERAL_ABOVE 0.20
 #define TFN_AUTO_FAST_BELOW 0.10
-#define TFN_AUTO_PROBE_FAST 8            // fast mode: read the counter back every 8th call
-#define TFN_AUTO_PROBE_GENERAL 32        // general mode: re-probe with the fast variant every 32nd call
+#define TFN_AUTO_PROBE_FAST 8            // fast / masked mode: read the counter back every 8th call
+#define TFN_AUTO_PROBE_GENERAL 32        // masked / general mode: every 32nd call probes the variant below
 
 namespace {
 
@@ -155,24 +159,37 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
             std::lock_guard<std::mutex> lk(h->auto_mu);
             if (!capturing && h->fb_pending && cudaEventQuery(h->fb_ev) == cudaSuccess) {
                 const double rate = h->fb_steps > 0 ? *h->fb_host / h->fb_steps : 0.0;
-                if (rate > TFN_AUTO_GENERAL_ABOVE) h->auto_general = 1;
-                else if (rate < TFN_AUTO_FAST_BELOW) h->auto_general = 0;
+                if (h->fb_variant == 0) {                 // probed the fast variant
+                    if (rate > TFN_AUTO_GENERAL_ABOVE) { if (h->auto_state == 0) h->auto_state = 1; }
+                    else if (rate < TFN_AUTO_FAST_BELOW) h->auto_state = 0;
+                } else {                                  // probed the masked variant
+                    if (rate > TFN_AUTO_GENERAL_ABOVE) h->auto_state = 2;
+                    else if (rate < TFN_AUTO_FAST_BELOW && h->auto_state == 2) h->auto_state = 1;
+                }
                 h->fb_pending = false;
             }
             cudaGetLastError();           // a not-ready query is not an error
             const unsigned n = h->auto_calls++;
-            const bool use_general = h->auto_general && (capturing || (n % TFN_AUTO_PROBE_GENERAL) != 0);
-            kernel = use_general ? tfn::TFN_KERNEL_STRIP_GENERAL : tfn::TFN_KERNEL_STRIP;
-            probe = !capturing && !use_general && h->fb_host && !h->fb_pending &&
-                    (h->auto_general || (n % TFN_AUTO_PROBE_FAST) == 0);
+            const bool can_probe = !capturing && h->fb_host && !h->fb_pending;
+            const bool reprobe = can_probe && (n % TFN_AUTO_PROBE_GENERAL) == 0;
+            int run = h->auto_state;      // 0 fast, 1 masked, 2 general
+            bool want = (n % TFN_AUTO_PROBE_FAST) == 0;
+            if (h->auto_state == 1 && reprobe) run = 0;             // is the data clean again?
+            if (h->auto_state == 2) { run = reprobe ? 1 : 2; want = reprobe; }
+            kernel = run == 0 ? tfn::TFN_KERNEL_STRIP : run == 1 ? tfn::TFN_KERNEL_STRIP_MASKED
+                                                                 : tfn::TFN_KERNEL_STRIP_GENERAL;
+            probe = can_probe && run != 2 && want;
+            if (probe) h->fb_variant = run;
         }
     }
-    // the fast strip variant is built for fp32 input without points; the general one has the
-    // same results (bit for bit) and runs everything else
-    if ((in_u16 || pts) && kernel == tfn::TFN_KERNEL_STRIP) kernel = tfn::TFN_KERNEL_STRIP_GENERAL;
-    const bool strip = (kernel == tfn::TFN_KERNEL_STRIP || kernel == tfn::TFN_KERNEL_STRIP_GENERAL);
+    // the fast and masked strip variants are built for fp32 input without points; the general
+    // one has the same results (bit for bit) and runs everything else
+    if ((in_u16 || pts) && (kernel == tfn::TFN_KERNEL_STRIP || kernel == tfn::TFN_KERNEL_STRIP_MASKED))
+        kernel = tfn::TFN_KERNEL_STRIP_GENERAL;
+    const bool strip = (kernel == tfn::TFN_KERNEL_STRIP || kernel == tfn::TFN_KERNEL_STRIP_GENERAL ||
+                        kernel == tfn::TFN_KERNEL_STRIP_MASKED);
     if (strip && !strip_ok) return TFN_ERR_INVALID_ARGUMENT;
-    const int gen = (kernel == tfn::TFN_KERNEL_STRIP_GENERAL) ? 1 : 0;
+    const int gen = (kernel == tfn::TFN_KERNEL_STRIP_GENERAL) ? 1 : (kernel == tfn::TFN_KERNEL_STRIP_MASKED) ? 2 : 0;
     int grid = 0;
     if (strip) {
         const int ctas_sm = in_u16 ? h->strip_ctas_u16 : h->strip_ctas_per_sm[gen][disp];
@@ -243,7 +260,7 @@ TFN_API int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_han
     h->mode = nz_mode;
     h->device = dev;
     h->sms = sms;
-    for (int g = 0; g < 2; ++g)
+    for (int g = 0; g < 3; ++g)
         for (int d = 0; d < 2; ++d) {
             int& n = h->strip_ctas_per_sm[g][d];
             n = tfn::strip_occupancy(filter, nz_mode, d != 0, g, 0);
@@ -283,7 +300,7 @@ TFN_API int tfn_set_option(tfn_handle h, int option, long long value) {
     if (!h) return TFN_ERR_INVALID_ARGUMENT;
     switch (option) {
     case TFN_OPT_KERNEL:
-        if (value < 0 || value > 3) return TFN_ERR_INVALID_ARGUMENT;
+        if (value < 0 || value > 4) return TFN_ERR_INVALID_ARGUMENT;
         h->kernel = (int)value;
         return TFN_OK;
     case TFN_OPT_STRIP_H:
@@ -522,7 +539,8 @@ TFN_API unsigned long long tfn_kernel_launches(void) { return g_launches.load();
 TFN_API int tfn_auto_variant(tfn_handle h, int* variant) {
     if (!h || !variant) return TFN_ERR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(h->auto_mu);
-    *variant = h->auto_general ? tfn::TFN_KERNEL_STRIP_GENERAL : tfn::TFN_KERNEL_STRIP;
+    *variant = h->auto_state == 2 ? tfn::TFN_KERNEL_STRIP_GENERAL
+             : h->auto_state == 1 ? tfn::TFN_KERNEL_STRIP_MASKED : tfn::TFN_KERNEL_STRIP;
     return TFN_OK;
 }
 

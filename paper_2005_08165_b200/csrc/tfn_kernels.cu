@@ -84,8 +84,9 @@ static cudaError_t launch_pixel(const KernelArgs& a0, bool disp, cudaStream_t st
 
 template <int F>
 static cudaError_t launch_f(const KernelArgs& a, int mode, bool disp, int kernel, int g, cudaStream_t st) {
-    if (kernel == TFN_KERNEL_STRIP || kernel == TFN_KERNEL_STRIP_GENERAL)
-        return launch_strip<F>(a, mode, disp, kernel == TFN_KERNEL_STRIP_GENERAL ? 1 : 0, g, st);
+    if (kernel == TFN_KERNEL_STRIP || kernel == TFN_KERNEL_STRIP_GENERAL || kernel == TFN_KERNEL_STRIP_MASKED)
+        return launch_strip<F>(a, mode, disp,
+                               kernel == TFN_KERNEL_STRIP_GENERAL ? 1 : kernel == TFN_KERNEL_STRIP_MASKED ? 2 : 0, g, st);
     return mode == MEAN ? launch_pixel<F, MEAN>(a, disp, st) : launch_pixel<F, MEDIAN>(a, disp, st);
 }
 

@@ -17,7 +17,8 @@
 
 namespace tfn {
 
-enum KernelId { TFN_KERNEL_AUTO = 0, TFN_KERNEL_PIXEL = 1, TFN_KERNEL_STRIP = 2, TFN_KERNEL_STRIP_GENERAL = 3 };
+enum KernelId { TFN_KERNEL_AUTO = 0, TFN_KERNEL_PIXEL = 1, TFN_KERNEL_STRIP = 2, TFN_KERNEL_STRIP_GENERAL = 3,
+                TFN_KERNEL_STRIP_MASKED = 4 };
 
 enum InDtype { TFN_IN_F32 = 0, TFN_IN_U16 = 1 };
 
@@ -45,7 +46,7 @@ cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, in
                         int grid_strip, cudaStream_t st);
 
 // resident CTAs per SM of the strip kernel variant (occupancy query)
-int strip_occupancy(int filter, int mode, bool disp, int variant, int in_u16);   // variant 0 fast, 1 general
+int strip_occupancy(int filter, int mode, bool disp, int variant, int in_u16);   // variant 0 fast, 1 general, 2 masked
 
 // per-filter strip instantiations (tfn_strip_<filter>.cu, compiled in parallel)
 template <int F>

@@ -168,24 +168,28 @@ __device__ __forceinline__ void load_raw(Slot& s, const StripCtx<unsigned short>
 // Q5 for the fast path: valid iff finite and >= FLT_MIN (rejects 0, negatives, NaN,
 // +-Inf, subnormals).  An invalid sample becomes NaN, which makes every candidate that
 // uses it NaN and so sends the pixel to the exact path.
+// VM (masked variant): the NaN carries the sign bit, so an OR of sample bits is negative
+// iff one of them is invalid (the special test below)
+template <bool VM> constexpr int bad_z() { return VM ? (int)0xffffffff : 0x7fffffff; }
+template <bool VM>
 __device__ __forceinline__ float sanitize_fast(float z, bool ok) {
     const bool good = valid_bits(z) & ok;      // no short circuit: FSEL, not a branch
-    return good ? z : __int_as_float(0x7fffffff);
+    return good ? z : __int_as_float(bad_z<VM>());
 }
 
-template <bool DISP, bool GEN, class T>
+template <bool DISP, bool GEN, class T, bool VM = false>
 __device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
     // the lane's own columns need only the value test; the halos are outside the image at
     // the first / last lane of a frame row; whole rows outside the image (loads predicated
     // off, stale registers) take a warp-uniform, rare branch — measured +1.9 % over
     // per-sample row predicates.  Lanes past W never store, so their stale samples need no NaN.
-    s.z[0] = sanitize_fast(s.raw[0], Ring<T, GEN>::on || c.okl);
+    s.z[0] = sanitize_fast<VM>(s.raw[0], Ring<T, GEN>::on || c.okl);
 #pragma unroll
-    for (int j = 1; j <= PPL; ++j) s.z[j] = valid_bits(s.raw[j]) ? s.raw[j] : __int_as_float(0x7fffffff);
-    s.z[PPL + 1] = sanitize_fast(s.raw[PPL + 1], Ring<T, GEN>::on || c.okr);
+    for (int j = 1; j <= PPL; ++j) s.z[j] = valid_bits(s.raw[j]) ? s.raw[j] : __int_as_float(bad_z<VM>());
+    s.z[PPL + 1] = sanitize_fast<VM>(s.raw[PPL + 1], Ring<T, GEN>::on || c.okr);
     if (!Ring<T, GEN>::on && __any_sync(0xffffffffu, !s.rok)) {
 #pragma unroll
-        for (int j = 0; j < PPL + 2; ++j) s.z[j] = s.rok ? s.z[j] : __int_as_float(0x7fffffff);
+        for (int j = 0; j < PPL + 2; ++j) s.z[j] = s.rok ? s.z[j] : __int_as_float(bad_z<VM>());
     }
     // exact for every valid sample; invalid ones give finite garbage here, but their
     // NaN z makes the pixel "special", which recomputes it exactly
@@ -288,7 +292,7 @@ __device__ __forceinline__ void store_packed(__half* o, const float* x, const fl
 // One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw holds row v+2 in
 // flight), C = slot(v) (C.raw receives row v+3), N = slot(v+1) (N.raw loaded; the rest
 // computed here).
-template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT>
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT, bool VM = false>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
                                          char* __restrict__ out, long long HW,
                                          unsigned colmask, float vf) {
@@ -302,7 +306,26 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     } else {
         load_raw(C, c, v + 3);                       // prefetch three rows ahead (C.raw is free)
     }
-    prepare<DISP, GEN>(N, c);
+    prepare<DISP, GEN, T, VM>(N, c);
+    // masked variant (VM): special (below) = Phi non-finite or zero at a pixel whose Q4 taps (all 9; FD: the plus)
+    // are valid.  An invalid sample is a NaN with the sign bit set, so the OR of the taps'
+    // bits is negative iff one is invalid — and then the fast path has already produced the
+    // canonical NaN (that tap's candidate is NaN).  Image borders (out-of-image taps) and
+    // lanes past W need no separate mask.
+    unsigned tapok = 0;
+    if (VM) {
+        int col[PPL + 2];
+#pragma unroll
+        for (int j = 0; j < PPL + 2; ++j)
+            col[j] = (Taps<F>::corners || (j >= 1 && j <= PPL))
+                         ? (__float_as_int(P.z[j]) | __float_as_int(C.z[j]) | __float_as_int(N.z[j])) : 0;
+#pragma unroll
+        for (int i = 0; i < PPL; ++i) {
+            const int taps = Taps<F>::corners ? (col[i] | col[i + 1] | col[i + 2])
+                                              : (__float_as_int(C.z[i]) | col[i + 1] | __float_as_int(C.z[i + 2]));
+            tapok |= (taps >= 0 ? 1u : 0u) << i;
+        }
+    }
 
     // ---- fp64 gradients (Eq. 15), oracle order (Q10) ----
     double gu[4], gv[4];
@@ -459,15 +482,23 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         // invalid centre poisons every candidate through m~ = m * NaN: the fast path
         // already wrote the canonical NaN).  Phi is NaN iff a candidate is non-finite (the
         // folds above), so one compare per pixel covers both.
-        const bool sp0 = !(fabsf(phi.x) > 0.f) && !isnan(zc2.x);
-        const bool sp1 = !(fabsf(phi.y) > 0.f) && !isnan(zc2.y);
-        special |= (sp0 ? (1u << i0) : 0u) | (sp1 ? (1u << i1) : 0u);
+        if (VM) {
+            const bool sp0 = !(fabsf(phi.x) > 0.f) && ((tapok >> i0) & 1u);
+            const bool sp1 = !(fabsf(phi.y) > 0.f) && ((tapok >> i1) & 1u);
+            special |= (sp0 ? (1u << i0) : 0u) | (sp1 ? (1u << i1) : 0u);
+        } else {
+            const bool sp0 = !(fabsf(phi.x) > 0.f) && !isnan(zc2.x);
+            const bool sp1 = !(fabsf(phi.y) > 0.f) && !isnan(zc2.y);
+            special |= (sp0 ? (1u << i0) : 0u) | (sp1 ? (1u << i1) : 0u);
+        }
     }
 
     // ---- known-invalid pixels (image border, columns past W) are never special: their
     //      out-of-image taps are NaN, so the fast path already produced the canonical NaN ----
-    const bool row_border = (v == 0) || (v == c.H - 1);
-    special &= row_border ? 0u : ~colmask;
+    if (!VM) {
+        const bool row_border = (v == 0) || (v == c.H - 1);
+        special &= row_border ? 0u : ~colmask;
+    }
     if (!GEN && __any_sync(0xffffffffu, special != 0)) {
         if (c.fired && (threadIdx.x & 31) == 0) atomicAdd(c.fired, 1);
         // rare: skipped candidates, flat / tie, invalid samples -> exact per-pixel path
@@ -529,7 +560,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
 }
 
 // Rows [ys, y1) of one strip: prologue, then the rolling window down the strip.
-template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT>
+template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT, bool VM = false>
 __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long long HW,
                                           unsigned colmask, int ys, int y1) {
     Slot S0, S1, S2;
@@ -544,15 +575,15 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
         __syncwarp();
         fetch_row(S0, c, ys - 1);
         fetch_row(S1, c, ys);
-        prepare<DISP, GEN>(S0, c);
-        prepare<DISP, GEN>(S1, c);
+        prepare<DISP, GEN, T, VM>(S0, c);
+        prepare<DISP, GEN, T, VM>(S1, c);
     } else {
         // prologue: rows ys-1 (S0), ys (S1) prepared; row ys+1 (S2) loaded
         load_raw(S0, c, ys - 1);
         load_raw(S1, c, ys);
         load_raw(S2, c, ys + 1);
-        prepare<DISP, GEN>(S0, c);
-        prepare<DISP, GEN>(S1, c);
+        prepare<DISP, GEN, T, VM>(S0, c);
+        prepare<DISP, GEN, T, VM>(S1, c);
         load_raw(S0, c, ys + 2);
     }
 #pragma unroll
@@ -566,11 +597,11 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
     }
     float vf = __int2float_rn(ys);      // exact row index as float (rows < 2^24)
     for (int v = ys; v < y1; v += 3) {
-        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S0, S1, S2, v, c, out, HW, colmask, vf);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT, VM>(S0, S1, S2, v, c, out, HW, colmask, vf);
         if (v + 1 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S1, S2, S0, v + 1, c, out, HW, colmask, vf + 1.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT, VM>(S1, S2, S0, v + 1, c, out, HW, colmask, vf + 1.0f);
         if (v + 2 >= y1) break;
-        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT>(S2, S0, S1, v + 2, c, out, HW, colmask, vf + 2.0f);
+        row_step<F, MODE, DISP, LAYOUT, GEN, T, PTS, OUT, VM>(S2, S0, S1, v + 2, c, out, HW, colmask, vf + 2.0f);
         vf += 3.0f;
     }
 }
@@ -578,8 +609,12 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
 // KV (kernel variant): 0 fast path + exact per-pixel special path, 1 general (no special
 // path: skips, flat, ties and invalid taps resolved in registers; ~45 % more instructions
 // per pixel, but no divergent exact-path calls — the better choice when many row steps
-// contain special pixels: holes, salt dropout, integer-quantized depth).  The fast variant
-// counts its special row steps into p.fired (host-side AUTO selection, tfn_abi.cu).
+// contain special pixels: holes, salt dropout, integer-quantized depth), 2 masked: the fast
+// variant whose special test also requires every Q4 tap to be valid — a pixel next to a hole
+// already comes out as the canonical NaN of the fast path, so holes and dropout no longer
+// send row steps to the exact path (config 4: 175 vs 164 Gpx/s general, 94 fast), at the
+// price of a tap-validity OR per row step (clean config 2: 189 vs 217 fast).  The fast and
+// masked variants count their special row steps into p.fired (host-side AUTO, tfn_abi.cu).
 template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS, int OUT>
 #ifdef TFN_STRIP_MAXNREG
 __global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(KernelArgs p) {
@@ -635,7 +670,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T, KV == 1>::on ? TFN_
         c.pts = p.pts ? p.pts + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm) : nullptr;
 
         c.y1 = y1;
-        strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS, OUT>(c, out, HW, colmask, y0, y1);
+        strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS, OUT, KV == 2>(c, out, HW, colmask, y0, y1);
         if (p.work) {
             int nxt = 0;
             if (lane == 0) nxt = atomicAdd(p.work, 1);

@@ -21,14 +21,15 @@ static cudaError_t launch_l(const KernelArgs& a, int grid, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-template <int F, int MODE, bool DISP>
+template <int F, int MODE, bool DISP, int KV = 0>
 static cudaError_t launch_fast(const KernelArgs& a, int grid, cudaStream_t st) {
-    return a.out_kind == 1 ? launch_l<F, MODE, DISP, 0, float, false, 1>(a, grid, st)
-         : a.out_kind == 2 ? launch_l<F, MODE, DISP, 0, float, false, 3>(a, grid, st)
-                           : launch_l<F, MODE, DISP, 0, float, false, 0>(a, grid, st);
+    return a.out_kind == 1 ? launch_l<F, MODE, DISP, KV, float, false, 1>(a, grid, st)
+         : a.out_kind == 2 ? launch_l<F, MODE, DISP, KV, float, false, 3>(a, grid, st)
+                           : launch_l<F, MODE, DISP, KV, float, false, 0>(a, grid, st);
 }
 
-// variant 0 = fast, 1 = general; uint16 input and points always run general
+// variant 0 = fast, 1 = general, 2 = masked (fast + tap-validity special test); uint16
+// input and points always run general
 template <int F, int MODE>
 static cudaError_t launch_m(const KernelArgs& a, bool disp, int variant, int grid, cudaStream_t st) {
     if (a.in_u16) {
@@ -39,8 +40,10 @@ static cudaError_t launch_m(const KernelArgs& a, bool disp, int variant, int gri
     if (a.pts)
         return disp ? launch_l<F, MODE, true, 1, float, true>(a, grid, st)
                     : launch_l<F, MODE, false, 1, float, true>(a, grid, st);
-    if (disp) return variant ? launch_l<F, MODE, true, 1, float>(a, grid, st) : launch_fast<F, MODE, true>(a, grid, st);
-    return variant ? launch_l<F, MODE, false, 1, float>(a, grid, st) : launch_fast<F, MODE, false>(a, grid, st);
+    if (disp) return variant == 1 ? launch_l<F, MODE, true, 1, float>(a, grid, st)
+                   : variant == 2 ? launch_fast<F, MODE, true, 2>(a, grid, st) : launch_fast<F, MODE, true>(a, grid, st);
+    return variant == 1 ? launch_l<F, MODE, false, 1, float>(a, grid, st)
+         : variant == 2 ? launch_fast<F, MODE, false, 2>(a, grid, st) : launch_fast<F, MODE, false>(a, grid, st);
 }
 
 template <int F>
@@ -61,8 +64,12 @@ static int occ(K kernel) {
 template <int F, int MODE>
 static int occ_m(bool disp, int variant, int in_u16) {
     if (in_u16) return occ(tfn_strip_kernel<F, MODE, false, 0, 1, unsigned short, false, 2>);
-    if (disp) return variant ? occ(tfn_strip_kernel<F, MODE, true, 0, 1, float, false, 2>) : occ(tfn_strip_kernel<F, MODE, true, 0, 0, float, false, 0>);
-    return variant ? occ(tfn_strip_kernel<F, MODE, false, 0, 1, float, false, 2>) : occ(tfn_strip_kernel<F, MODE, false, 0, 0, float, false, 0>);
+    if (disp) return variant == 1 ? occ(tfn_strip_kernel<F, MODE, true, 0, 1, float, false, 2>)
+                   : variant == 2 ? occ(tfn_strip_kernel<F, MODE, true, 0, 2, float, false, 0>)
+                                  : occ(tfn_strip_kernel<F, MODE, true, 0, 0, float, false, 0>);
+    return variant == 1 ? occ(tfn_strip_kernel<F, MODE, false, 0, 1, float, false, 2>)
+         : variant == 2 ? occ(tfn_strip_kernel<F, MODE, false, 0, 2, float, false, 0>)
+                        : occ(tfn_strip_kernel<F, MODE, false, 0, 0, float, false, 0>);
 }
 
 template <int F>

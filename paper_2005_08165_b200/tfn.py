@@ -24,7 +24,7 @@ TFN_OK, TFN_ERR_INVALID_ARGUMENT, TFN_ERR_CONFIG, TFN_ERR_CUDA = 0, 1, 2, 3
 FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3, "custom": 4}
 MODES = {"mean": 0, "median": 1}
 LAYOUTS = {"planar": 0, "packed": 1}
-KERNELS = {"auto": 0, "pixel": 1, "strip": 2, "general": 3}
+KERNELS = {"auto": 0, "pixel": 1, "strip": 2, "general": 3, "masked": 4}
 OUT_DTYPES = {"f32": 0, "f16": 1, "oct16": 2}
 OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_DYNAMIC, OPT_OUT_DTYPE = 0, 1, 2, 3, 4
 

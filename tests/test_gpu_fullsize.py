@@ -83,14 +83,14 @@ def test_full_size_config3_disparity(tfn):
             sampled(out[fi], frame, ts.K_VGA, "scharr", "median", rng, disp=True)
 
 
-def test_full_size_config4_holes_auto_general(tfn):
+def test_full_size_config4_holes_auto_masked(tfn):
     from paper_2005_08165_b200 import tfn as T
     n, H, W = 128, 1080, 1920
     sc = ts.random_scenes(n, ts.K_1080, H, W, seed=0, holes=True, salt=0.01)
     z = render_gpu(sc, ts.K_1080, H, W, n, chunk=16)
     est = tfn.Estimator(ts.K_1080, "prewitt", "median")
     warm(est, lambda: est.estimate(z), n=8)
-    assert T.tfn_auto_variant(est.h) == 3           # the bench launch runs the general variant
+    assert T.tfn_auto_variant(est.h) == 4           # the bench launch runs the masked variant
     out = est.estimate(z).cpu().numpy()
     rng = np.random.default_rng(4)
     for i, fi in enumerate((0, 64, 127)):

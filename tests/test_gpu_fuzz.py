@@ -32,7 +32,7 @@ def test_white_noise_depth(tfn, seed):
     x = torch.from_numpy(z).cuda()
     for f in ("fd", "sobel", "scharr", "prewitt", (0.7, 2.9)):
         for m in ("mean", "median"):
-            outs = [tfn.Estimator(K, f, m, kernel=k).estimate(x).cpu().numpy() for k in ("strip", "general", "pixel")]
+            outs = [tfn.Estimator(K, f, m, kernel=k).estimate(x).cpu().numpy() for k in ("strip", "masked", "general", "pixel")]
             for o in outs[1:]:
                 assert np.array_equal(outs[0].view(np.uint32), o.view(np.uint32)), (seed, f, m)
             assert_parity(compare(outs[0], oracle.estimate(z, K, f, m), z, K), f"fuzz {seed} {f}/{m}")

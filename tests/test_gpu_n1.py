@@ -87,7 +87,7 @@ def test_u16_bitwise_equals_f32_of_codes(tfn):
     for f in FILTERS:
         for m in MODES:
             ref = run_f32(tfn, zf, ts.K_VGA, f, m, kernel="pixel")
-            for kernel in ("auto", "strip", "general", "pixel"):
+            for kernel in ("auto", "strip", "masked", "general", "pixel"):
                 assert same_bits(run_u16(tfn, codes, ts.K_VGA, f, m, kernel=kernel), ref), (f, m, kernel)
             pk = run_u16(tfn, codes, ts.K_VGA, f, m, layout="packed")
             assert same_bits(pk.permute(0, 3, 1, 2).contiguous(), ref), (f, m, "packed")
@@ -107,7 +107,7 @@ def test_f16_output_is_rounded_f32(tfn):
     z = ts.render(sc, ts.K_VGA, 480, 640).depth.numpy()
     codes = mm_codes(frames=2, seed=9)
     for layout in ("planar", "packed"):
-        for kernel in ("auto", "strip", "general", "pixel"):
+        for kernel in ("auto", "strip", "masked", "general", "pixel"):
             for f, m in (("sobel", "median"), ("fd", "mean")):
                 a = run_f32(tfn, z, ts.K_VGA, f, m, kernel=kernel, layout=layout).numpy()
                 h = run_f32(tfn, z, ts.K_VGA, f, m, kernel=kernel, layout=layout, out_dtype="f16").numpy()
@@ -153,7 +153,7 @@ def test_oct16_normals(tfn):
     ref32 = run_f32(tfn, z.numpy(), ts.K_VGA, "sobel", "median").numpy()
     base = None
     for layout in ("planar", "packed"):
-        for kernel in ("auto", "strip", "general", "pixel"):
+        for kernel in ("auto", "strip", "masked", "general", "pixel"):
             q = run_f32(tfn, z.numpy(), ts.K_VGA, "sobel", "median", kernel=kernel, layout=layout,
                         out_dtype="oct16")
             assert q.dtype == torch.int16 and q.shape == ((2, 2, 480, 640) if layout == "planar" else (2, 480, 640, 2))

@@ -403,10 +403,30 @@ def test_general_kernel_bitwise_vs_pixel(tfn, cfg1, random8):
             check(tfn, z, ts.K_VGA, f, m, kernel="general")
 
 
+def test_masked_kernel_bitwise_vs_pixel(tfn, cfg1, random8):
+    """kernel=4 (the fast kernel whose special path skips pixels with an invalid Q4 tap —
+    their NaN is already exact — and needs no border masks: out-of-image taps are invalid
+    taps) is bit-identical to the per-pixel kernel on every hard case, both layouts."""
+    for name, z, K, disp in _general_cases(cfg1, random8):
+        for f in FILTERS:
+            for m in MODES:
+                gp = run_gpu(tfn, z, K, f, m, disp=disp, kernel="pixel")
+                gm = run_gpu(tfn, z, K, f, m, disp=disp, kernel="masked")
+                assert np.array_equal(gm.view(np.uint32), gp.view(np.uint32)), (name, f, m)
+                gk = run_gpu(tfn, z, K, f, m, disp=disp, kernel="masked", layout="packed")
+                assert np.array_equal(gm.view(np.uint32), gk.view(np.uint32)), (name, f, m, "packed")
+                if f == "sobel" and m == "median":
+                    for sh in (5, 13):
+                        gs = run_gpu(tfn, z, K, f, m, disp=disp, kernel="masked", strip_h=sh)
+                        assert np.array_equal(gm.view(np.uint32), gs.view(np.uint32)), (name, sh)
+
+
 def test_auto_variant_follows_the_special_rate(tfn, cfg1):
-    """AUTO starts on the fast strip kernel, moves to the general one on hole-heavy input
-    (config-4 style: ~98 % of row steps need the special path) and back on clean input;
-    the output is bit-identical whichever variant ran."""
+    """AUTO starts on the fast strip kernel; on hole-heavy input (config-4 style: ~98 % of the
+    fast kernel's row steps need the special path, few of the masked kernel's) it moves to
+    the masked kernel; on millimetre-quantized depth (dZ = 0 everywhere, the masked kernel
+    fires too) on to the general one; and it stays fast on clean input.  The output is
+    bit-identical whichever variant ran."""
     from paper_2005_08165_b200 import tfn as T
     sc = ts.random_scenes(2, ts.K_1080, 1080, 1920, seed=7, holes=True, salt=0.01)
     holes = ts.render(sc, ts.K_1080, 1080, 1920).depth.cuda()
@@ -417,7 +437,15 @@ def test_auto_variant_follows_the_special_rate(tfn, cfg1):
         out = est.estimate(holes)
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
-    assert T.tfn_auto_variant(est.h) == 3
+    assert T.tfn_auto_variant(est.h) == 4
+    quant = torch.round(holes * 1000.0) / 1000.0          # fp32 millimetre steps: dZ = 0 is common
+    refq = run_gpu(tfn, quant.cpu().numpy(), ts.K_1080, "sobel", "median", kernel="pixel")
+    estq = tfn.Estimator(ts.K_1080, "sobel", "median")
+    for _ in range(80):
+        out = estq.estimate(quant)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), refq.view(np.uint32))
+    assert T.tfn_auto_variant(estq.h) == 3
     clean = cfg1.depth.reshape(1, 480, 640).repeat(4, 1, 1).cuda()
     est2 = tfn.Estimator(ts.K_VGA, "sobel", "median")
     for _ in range(40):
@@ -435,7 +463,7 @@ def test_noisy_depth_parity(tfn, random8, level):
     for f in ("fd", "sobel"):
         for m in MODES:
             g, _ = check(tfn, z, ts.K_VGA, f, m)
-            for kernel in ("strip", "general", "pixel"):
+            for kernel in ("strip", "masked", "general", "pixel"):
                 gk = run_gpu(tfn, z, ts.K_VGA, f, m, kernel=kernel)
                 assert np.array_equal(g.view(np.uint32), gk.view(np.uint32)), (level, f, m, kernel)
 
@@ -468,7 +496,7 @@ def test_custom_weights_parity(tfn, random8, w):
     for m in MODES:
         for x in (z, zq):
             g, _ = check(tfn, x, ts.K_VGA, w, m)
-            for kernel in ("strip", "general", "pixel"):
+            for kernel in ("strip", "masked", "general", "pixel"):
                 gk = run_gpu(tfn, x, ts.K_VGA, w, m, kernel=kernel)
                 assert np.array_equal(g.view(np.uint32), gk.view(np.uint32)), (w, m, kernel)
 
@@ -549,7 +577,7 @@ def test_extreme_depth_scales_and_occlusions(tfn, random8, scale):
         for f in ("fd", "sobel"):
             for m in MODES:
                 g, _ = check(tfn, z, K, f, m)
-                for kernel in ("general", "pixel"):
+                for kernel in ("masked", "general", "pixel"):
                     gk = run_gpu(tfn, z, K, f, m, kernel=kernel)
                     assert np.array_equal(g.view(np.uint32), gk.view(np.uint32)), (scale, K, f, m, kernel)
 
