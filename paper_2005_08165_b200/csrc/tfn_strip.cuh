@@ -52,6 +52,8 @@ struct Slot {
     double w[6];       // x = 1/z (depth) or d (disparity), fp64
     double head[4];    // kp*D_h(row-1) + k0*D_h(row)   (D_h re-derived from w when needed)
     float rN[4], rNW[4], rNE[4];   // pair reciprocals of the N / NW / NE neighbours (pairs owned by the row above)
+    unsigned hb;       // masked variant: byte i bit 7 set iff a sample of columns i..i+2 is invalid
+    unsigned cb;       //   (FD) byte i bit 7 set iff the sample of column i+1 is invalid
 };
 
 template <class T>
@@ -191,6 +193,16 @@ __device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
 #pragma unroll
         for (int j = 0; j < PPL + 2; ++j) s.z[j] = s.rok ? s.z[j] : __int_as_float(bad_z<VM>());
     }
+    if (VM && PPL == 4) {
+        // an invalid sample is a NaN with the sign bit set: OR the row's 3-column windows and
+        // gather the four sign bytes (PRMT) — the tap test of the masked variant's vote
+        int h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __float_as_int(s.z[i]) | __float_as_int(s.z[i + 1]) | __float_as_int(s.z[i + 2]);
+        s.hb = __byte_perm(__byte_perm(h[0], h[1], 0x0073), __byte_perm(h[2], h[3], 0x0073), 0x5410) & 0x80808080u;
+        s.cb = __byte_perm(__byte_perm(__float_as_int(s.z[1]), __float_as_int(s.z[2]), 0x0073),
+                           __byte_perm(__float_as_int(s.z[3]), __float_as_int(s.z[4]), 0x0073), 0x5410) & 0x80808080u;
+    }
     // exact for every valid sample; invalid ones give finite garbage here, but their
     // NaN z makes the pixel "special", which recomputes it exactly
 #pragma unroll
@@ -314,17 +326,10 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     // lanes past W need no separate mask.
     unsigned tapok = 0;
     if (VM) {
-        int col[PPL + 2];
+        // all 9 taps (FD: the plus) valid <=> no sign byte set in the rows' window masks
+        const unsigned bad = Taps<F>::corners ? (P.hb | C.hb | N.hb) : (C.hb | P.cb | N.cb);
 #pragma unroll
-        for (int j = 0; j < PPL + 2; ++j)
-            col[j] = (Taps<F>::corners || (j >= 1 && j <= PPL))
-                         ? (__float_as_int(P.z[j]) | __float_as_int(C.z[j]) | __float_as_int(N.z[j])) : 0;
-#pragma unroll
-        for (int i = 0; i < PPL; ++i) {
-            const int taps = Taps<F>::corners ? (col[i] | col[i + 1] | col[i + 2])
-                                              : (__float_as_int(C.z[i]) | col[i + 1] | __float_as_int(C.z[i + 2]));
-            tapok |= (taps >= 0 ? 1u : 0u) << i;
-        }
+        for (int i = 0; i < PPL; ++i) tapok |= ((bad >> (8 * i + 7)) & 1u ? 0u : 1u) << i;
     }
 
     // ---- fp64 gradients (Eq. 15), oracle order (Q10) ----
@@ -612,8 +617,8 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
 // contain special pixels: holes, salt dropout, integer-quantized depth), 2 masked: the fast
 // variant whose special test also requires every Q4 tap to be valid — a pixel next to a hole
 // already comes out as the canonical NaN of the fast path, so holes and dropout no longer
-// send row steps to the exact path (config 4: 175 vs 164 Gpx/s general, 94 fast), at the
-// price of a tap-validity OR per row step (clean config 2: 189 vs 217 fast).  The fast and
+// send row steps to the exact path (config 4: 186 vs 164 Gpx/s general, 94 fast), at the
+// price of per-row tap-validity masks (clean config 2: 204 vs 217 fast).  The fast and
 // masked variants count their special row steps into p.fired (host-side AUTO, tfn_abi.cu).
 template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS, int OUT>
 #ifdef TFN_STRIP_MAXNREG
