@@ -481,10 +481,27 @@ def main():
         if pg:
             pg.all_reduce(tt, op=pg.ReduceOp.MAX)
         dt = float(tt.item())
+        bi, bo = int(hin.numel() * hin.element_size()), int(hout.numel() * hout.element_size())
         e2e = {"value": per_rank * H * W * args.e2e_steps * ws / dt / 1e6, "unit": "Mpixel/s",
-               "h2d_bytes_per_step": int(hin.numel() * hin.element_size()),
-               "d2h_bytes_per_step": int(hout.numel() * hout.element_size()),
+               "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                "api": "tfn_estimate_host (pinned host buffers, chunked H2D/kernel/D2H on 2 streams)"}
+        # the link bound of this call: plain pinned copies of the same buffers, timed alone;
+        # with H2D and D2H overlapped the call cannot beat the slower direction
+        try:
+            def _copy_s(dst, src):
+                torch.cuda.synchronize()
+                c0 = time.perf_counter()
+                dst.copy_(src)
+                torch.cuda.synchronize()
+                return time.perf_counter() - c0
+            t_in = min(_copy_s(x, hin) for _ in range(2))
+            t_out = min(_copy_s(hout, out) for _ in range(2))
+            bound = per_rank * H * W / max(t_in, t_out) / 1e6
+            e2e["link"] = {"h2d_GBps": round(bi / t_in / 1e9, 1), "d2h_GBps": round(bo / t_out / 1e9, 1),
+                           "bound_Mpx_s": bound, "frac": e2e["value"] / ws / bound,
+                           "what": "pinned copies of the same buffers timed alone on this rank"}
+        except Exception:                       # the copies are context, never the measurement
+            pass
         del hin, hout
 
     cpu = None
