@@ -64,9 +64,9 @@ struct tfn_ctx {
 #define TFN_WORK_RING 4096
 // AUTO: step to the next variant (fast -> masked -> general) when more than this fraction
 // of the probed variant's row steps needed the special path (measured break-even ~0.24:
-// config 2 has 0.011 and runs 217 fast vs 204 masked vs 167 general; config 4 (holes + 1 %
+// config 2 has 0.011 and runs 217 fast vs 210 masked vs 167 general; config 4 (holes + 1 %
 // salt) fires on 0.98 of the fast variant's row steps but few of the masked one's, and
-// runs 94 fast vs 186 masked vs 164 general); back below TFN_AUTO_FAST_BELOW
+// runs 94 fast vs 191 masked vs 164 general); back below TFN_AUTO_FAST_BELOW
 #define TFN_AUTO_GENERAL_ABOVE 0.20
 #define TFN_AUTO_FAST_BELOW 0.10
 #define TFN_AUTO_PROBE_FAST 8            // fast / masked mode: read the counter back every 8th call

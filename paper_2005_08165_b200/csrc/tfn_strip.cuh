@@ -328,8 +328,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     if (VM) {
         // all 9 taps (FD: the plus) valid <=> no sign byte set in the rows' window masks
         const unsigned bad = Taps<F>::corners ? (P.hb | C.hb | N.hb) : (C.hb | P.cb | N.cb);
-#pragma unroll
-        for (int i = 0; i < PPL; ++i) tapok |= ((bad >> (8 * i + 7)) & 1u ? 0u : 1u) << i;
+        tapok = ~bad;                // bit 8i+7 set iff pixel i's taps are all valid
     }
 
     // ---- fp64 gradients (Eq. 15), oracle order (Q10) ----
@@ -488,8 +487,8 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         // already wrote the canonical NaN).  Phi is NaN iff a candidate is non-finite (the
         // folds above), so one compare per pixel covers both.
         if (VM) {
-            const bool sp0 = !(fabsf(phi.x) > 0.f) && ((tapok >> i0) & 1u);
-            const bool sp1 = !(fabsf(phi.y) > 0.f) && ((tapok >> i1) & 1u);
+            const bool sp0 = !(fabsf(phi.x) > 0.f) && (tapok & (0x80u << (8 * i0)));
+            const bool sp1 = !(fabsf(phi.y) > 0.f) && (tapok & (0x80u << (8 * i1)));
             special |= (sp0 ? (1u << i0) : 0u) | (sp1 ? (1u << i1) : 0u);
         } else {
             const bool sp0 = !(fabsf(phi.x) > 0.f) && !isnan(zc2.x);
@@ -617,8 +616,8 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
 // contain special pixels: holes, salt dropout, integer-quantized depth), 2 masked: the fast
 // variant whose special test also requires every Q4 tap to be valid — a pixel next to a hole
 // already comes out as the canonical NaN of the fast path, so holes and dropout no longer
-// send row steps to the exact path (config 4: 186 vs 164 Gpx/s general, 94 fast), at the
-// price of per-row tap-validity masks (clean config 2: 204 vs 217 fast).  The fast and
+// send row steps to the exact path (config 4: 191 vs 164 Gpx/s general, 94 fast), at the
+// price of per-row tap-validity masks (clean config 2: 210 vs 217 fast).  The fast and
 // masked variants count their special row steps into p.fired (host-side AUTO, tfn_abi.cu).
 template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS, int OUT>
 #ifdef TFN_STRIP_MAXNREG
