@@ -199,9 +199,10 @@ __device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
         int h[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) h[i] = __float_as_int(s.z[i]) | __float_as_int(s.z[i + 1]) | __float_as_int(s.z[i + 2]);
-        s.hb = __byte_perm(__byte_perm(h[0], h[1], 0x0073), __byte_perm(h[2], h[3], 0x0073), 0x5410) & 0x80808080u;
+        // (only bit 7 of each byte is ever tested: the other bits are left as gathered)
+        s.hb = __byte_perm(__byte_perm(h[0], h[1], 0x0073), __byte_perm(h[2], h[3], 0x0073), 0x5410);
         s.cb = __byte_perm(__byte_perm(__float_as_int(s.z[1]), __float_as_int(s.z[2]), 0x0073),
-                           __byte_perm(__float_as_int(s.z[3]), __float_as_int(s.z[4]), 0x0073), 0x5410) & 0x80808080u;
+                           __byte_perm(__float_as_int(s.z[3]), __float_as_int(s.z[4]), 0x0073), 0x5410);
     }
     // exact for every valid sample; invalid ones give finite garbage here, but their
     // NaN z makes the pixel "special", which recomputes it exactly
