@@ -407,6 +407,10 @@ def test_masked_kernel_bitwise_vs_pixel(tfn, cfg1, random8):
     """kernel=4 (the fast kernel whose special path skips pixels with an invalid Q4 tap —
     their NaN is already exact — and needs no border masks: out-of-image taps are invalid
     taps) is bit-identical to the per-pixel kernel on every hard case, both layouts."""
+    from paper_2005_08165_b200 import tfn as T
+    est = tfn.Estimator(ts.K_VGA, "sobel", "median")
+    with pytest.raises(T.TfnError):
+        T.tfn_set_option(est.h, T.OPT_KERNEL, 5)          # 0 auto .. 4 masked
     for name, z, K, disp in _general_cases(cfg1, random8):
         for f in FILTERS:
             for m in MODES:
