@@ -17,7 +17,7 @@
 //   fp32:  one MUFU reciprocal per neighbour PAIR (shared by both pixels of the pair),
 //          tau = fma(m Z_c, R, +-m), Phi (24-op median network / mean), n_z, normalise,
 //          orient — packed FMUL2/FFMA2/FADD2 over pixel pairs (0,1), (2,3).
-// Two variants (KV):
+// Three variants (KV), bit-identical, picked at run time by AUTO (tfn_abi.cu):
 //   fast (0):    all 8 candidates finite and Phi != 0 (no skips, no flat rule, no
 //                orientation tie, valid pixel) in registers; anything else ("special":
 //                holes, invalid samples, dZ == 0, flat, ties) runs the exact per-pixel
@@ -26,7 +26,10 @@
 //                writes the canonical NaN.
 //   general (1): no special path — invalid samples get NaN fp64 x (F2F), skipped
 //                candidates are padded in registers (phi_any), flat / none / ties /
-//                invalid resolved by finish_tail: the per-pixel kernel's code, inline.
+//                invalid resolved by finish_tail2: the per-pixel kernel's arithmetic.
+//   masked (2):  the fast variant whose special test also requires every Q4 tap to be
+//                valid (per-row sign-byte masks of the sanitized samples): a pixel beside
+//                a hole is already the canonical NaN, so holes and dropout stay fast.
 #pragma once
 
 #ifndef TFN_U16_MINBLOCKS
