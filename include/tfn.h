@@ -208,8 +208,8 @@ unsigned long long tfn_kernel_launches(void);
  * strip kernel).  AUTO starts fast; the fast and masked kernels count the row steps that
  * needed their special path, the count returns asynchronously (pinned word + event, read at
  * a later call, never a sync), and above 20 % of row steps AUTO steps fast -> masked ->
- * general (below 10 % back; masked / general mode re-probe the variant below every 32nd
- * call).  Results are bit-identical either way; only speed differs.
+ * general (below 10 % back; masked mode re-probes the fast kernel every 256th call,
+ * general mode the masked one every 32nd).  Results are bit-identical either way; only speed differs.
  * uint16 input and the point cloud always run the general kernel.  Returns
  * TFN_ERR_INVALID_ARGUMENT for NULLs. */
 int tfn_auto_variant(tfn_handle h, int* variant);

@@ -70,7 +70,9 @@ struct tfn_ctx {
 #define TFN_AUTO_GENERAL_ABOVE 0.20
 #define TFN_AUTO_FAST_BELOW 0.10
 #define TFN_AUTO_PROBE_FAST 8            // fast / masked mode: read the counter back every 8th call
-#define TFN_AUTO_PROBE_GENERAL 32        // masked / general mode: every 32nd call probes the variant below
+#define TFN_AUTO_PROBE_GENERAL 32        // general mode: every 32nd call probes the masked variant
+#define TFN_AUTO_PROBE_MASKED 256        // masked mode: every 256th call probes the fast variant (on
+                                         // holey data a fast call costs ~2x; back to fast gains ~3 %)
 
 namespace {
 
@@ -171,11 +173,14 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
             cudaGetLastError();           // a not-ready query is not an error
             const unsigned n = h->auto_calls++;
             const bool can_probe = !capturing && h->fb_host && !h->fb_pending;
-            const bool reprobe = can_probe && (n % TFN_AUTO_PROBE_GENERAL) == 0;
             int run = h->auto_state;      // 0 fast, 1 masked, 2 general
             bool want = (n % TFN_AUTO_PROBE_FAST) == 0;
-            if (h->auto_state == 1 && reprobe) run = 0;             // is the data clean again?
-            if (h->auto_state == 2) { run = reprobe ? 1 : 2; want = reprobe; }
+            if (h->auto_state == 1 && can_probe && (n % TFN_AUTO_PROBE_MASKED) == 0) run = 0;   // clean again?
+            if (h->auto_state == 2) {
+                const bool reprobe = can_probe && (n % TFN_AUTO_PROBE_GENERAL) == 0;
+                run = reprobe ? 1 : 2;
+                want = reprobe;
+            }
             kernel = run == 0 ? tfn::TFN_KERNEL_STRIP : run == 1 ? tfn::TFN_KERNEL_STRIP_MASKED
                                                                  : tfn::TFN_KERNEL_STRIP_GENERAL;
             probe = can_probe && run != 2 && want;
