@@ -214,6 +214,15 @@ unsigned long long tfn_kernel_launches(void);
  * TFN_ERR_INVALID_ARGUMENT for NULLs. */
 int tfn_auto_variant(tfn_handle h, int* variant);
 
+/* Host-only probe of the AUTO state machine (no device needed; for tests): states 0 fast,
+ * 1 masked, 2 general.  *next_state = the state after a probe of variant `probed` (0 fast,
+ * 1 masked) reported `rate` (fraction of its row steps that needed the special path);
+ * *run (0/1/2) and *probe (0/1) = the variant call number `call` runs in `state` and whether
+ * it counts its special row steps, when a read-back is possible (`can_probe`).  Returns
+ * TFN_ERR_INVALID_ARGUMENT for NULL outputs or states / variants out of range. */
+int tfn_debug_auto(int state, int probed, double rate, unsigned call, int can_probe,
+                   int* next_state, int* run, int* probe);
+
 /* ABI version (major*10000 + minor*100 + patch). */
 int tfn_version(void);
 

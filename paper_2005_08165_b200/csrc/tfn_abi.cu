@@ -75,6 +75,36 @@ struct tfn_ctx {
                                          // holey data a fast call costs ~2x; back to fast gains ~3 %)
 
 namespace {
+// AUTO state machine, pure host logic (pinned by tests/test_abi.py through tfn_debug_auto).
+// state: 0 fast, 1 masked, 2 general.  auto_next: the state after the feedback of a probe
+// of `probed` (0 fast, 1 masked) that fired on `rate` of its row steps.
+int auto_next(int state, int probed, double rate) {
+    if (probed == 0) {
+        if (rate > TFN_AUTO_GENERAL_ABOVE) return state == 0 ? 1 : state;
+        if (rate < TFN_AUTO_FAST_BELOW) return 0;
+        return state;
+    }
+    if (rate > TFN_AUTO_GENERAL_ABOVE) return 2;
+    if (rate < TFN_AUTO_FAST_BELOW && state == 2) return 1;
+    return state;
+}
+// auto_pick: the variant call n runs in `state` (0 fast, 1 masked, 2 general) and whether it
+// counts its special row steps (a probe), given whether a probe can be read back
+void auto_pick(int state, unsigned n, bool can_probe, int* run, bool* probe) {
+    int r = state;
+    bool want = (n % TFN_AUTO_PROBE_FAST) == 0;
+    if (state == 1 && can_probe && (n % TFN_AUTO_PROBE_MASKED) == 0) r = 0;   // clean again?
+    if (state == 2) {
+        const bool reprobe = can_probe && (n % TFN_AUTO_PROBE_GENERAL) == 0;
+        r = reprobe ? 1 : 2;
+        want = reprobe;
+    }
+    *run = r;
+    *probe = can_probe && r != 2 && want;
+}
+}  // namespace
+
+namespace {
 
 bool is_fin(double x) { return std::isfinite(x); }
 
@@ -161,29 +191,16 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
             std::lock_guard<std::mutex> lk(h->auto_mu);
             if (!capturing && h->fb_pending && cudaEventQuery(h->fb_ev) == cudaSuccess) {
                 const double rate = h->fb_steps > 0 ? *h->fb_host / h->fb_steps : 0.0;
-                if (h->fb_variant == 0) {                 // probed the fast variant
-                    if (rate > TFN_AUTO_GENERAL_ABOVE) { if (h->auto_state == 0) h->auto_state = 1; }
-                    else if (rate < TFN_AUTO_FAST_BELOW) h->auto_state = 0;
-                } else {                                  // probed the masked variant
-                    if (rate > TFN_AUTO_GENERAL_ABOVE) h->auto_state = 2;
-                    else if (rate < TFN_AUTO_FAST_BELOW && h->auto_state == 2) h->auto_state = 1;
-                }
+                h->auto_state = auto_next(h->auto_state, h->fb_variant, rate);
                 h->fb_pending = false;
             }
             cudaGetLastError();           // a not-ready query is not an error
             const unsigned n = h->auto_calls++;
             const bool can_probe = !capturing && h->fb_host && !h->fb_pending;
-            int run = h->auto_state;      // 0 fast, 1 masked, 2 general
-            bool want = (n % TFN_AUTO_PROBE_FAST) == 0;
-            if (h->auto_state == 1 && can_probe && (n % TFN_AUTO_PROBE_MASKED) == 0) run = 0;   // clean again?
-            if (h->auto_state == 2) {
-                const bool reprobe = can_probe && (n % TFN_AUTO_PROBE_GENERAL) == 0;
-                run = reprobe ? 1 : 2;
-                want = reprobe;
-            }
+            int run = 0;
+            auto_pick(h->auto_state, n, can_probe, &run, &probe);
             kernel = run == 0 ? tfn::TFN_KERNEL_STRIP : run == 1 ? tfn::TFN_KERNEL_STRIP_MASKED
                                                                  : tfn::TFN_KERNEL_STRIP_GENERAL;
-            probe = can_probe && run != 2 && want;
             if (probe) h->fb_variant = run;
         }
     }
@@ -546,6 +563,17 @@ TFN_API int tfn_auto_variant(tfn_handle h, int* variant) {
     std::lock_guard<std::mutex> lk(h->auto_mu);
     *variant = h->auto_state == 2 ? tfn::TFN_KERNEL_STRIP_GENERAL
              : h->auto_state == 1 ? tfn::TFN_KERNEL_STRIP_MASKED : tfn::TFN_KERNEL_STRIP;
+    return TFN_OK;
+}
+
+TFN_API int tfn_debug_auto(int state, int probed, double rate, unsigned call, int can_probe,
+                           int* next_state, int* run, int* probe) {
+    if (!next_state || !run || !probe || state < 0 || state > 2 || probed < 0 || probed > 1)
+        return TFN_ERR_INVALID_ARGUMENT;
+    *next_state = auto_next(state, probed, rate);
+    bool pr = false;
+    auto_pick(state, call, can_probe != 0, run, &pr);
+    *probe = pr ? 1 : 0;
     return TFN_OK;
 }
 

@@ -34,6 +34,7 @@ ABI_SYMBOLS = (
     "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8", "tfn_destroy", "tfn_status_string",
     "tfn_kernel_launches", "tfn_version", "tfn_debug_sol", "tfn_auto_variant", "tfn_estimate_u16",
     "tfn_estimate_host_u16", "tfn_estimate_points", "tfn_set_filter_weights", "tfn_plane_fit",
+    "tfn_debug_auto",
 )
 PLANE_METHODS = {"pca": 0, "svd": 1}
 INPUT_KINDS = {"depth": 0, "disparity": 1, "depth_u16": 2}
@@ -78,6 +79,8 @@ def lib() -> ctypes.CDLL:
         L.tfn_debug_sol.argtypes = [vp, i, i, i, vp, vp]
         L.tfn_destroy.argtypes = [vp]
         L.tfn_auto_variant.argtypes = [vp, ctypes.POINTER(i)]
+        L.tfn_debug_auto.argtypes = [i, i, d, ctypes.c_uint, i, ctypes.POINTER(i), ctypes.POINTER(i),
+                                     ctypes.POINTER(i)]
         L.tfn_status_string.argtypes = [i]
         L.tfn_status_string.restype = ctypes.c_char_p
         L.tfn_kernel_launches.restype = ctypes.c_ulonglong
@@ -89,7 +92,8 @@ def lib() -> ctypes.CDLL:
                                                      "tfn_destroy", "tfn_version", "tfn_debug_sol",
                                                      "tfn_auto_variant", "tfn_estimate_u16",
                                                      "tfn_estimate_host_u16", "tfn_estimate_points",
-                                                     "tfn_set_filter_weights", "tfn_plane_fit"):
+                                                     "tfn_set_filter_weights", "tfn_plane_fit",
+                                                     "tfn_debug_auto"):
                 f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -196,10 +200,19 @@ def tfn_version() -> int:
 
 
 def tfn_auto_variant(h: int) -> int:
-    """The strip variant AUTO currently picks for handle h: 2 fast, 3 general."""
+    """The strip variant AUTO currently picks for handle h: 2 fast, 4 masked, 3 general."""
     v = ctypes.c_int(0)
     _check(lib().tfn_auto_variant(h, ctypes.byref(v)), "tfn_auto_variant")
     return v.value
+
+
+def tfn_debug_auto(state: int, probed: int, rate: float, call: int, can_probe: bool):
+    """Host-only AUTO state machine probe: (next_state, run, probe) — states / runs 0 fast,
+    1 masked, 2 general (include/tfn.h)."""
+    ns, run, pr = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    _check(lib().tfn_debug_auto(state, probed, rate, call, int(can_probe), ctypes.byref(ns), ctypes.byref(run),
+                                ctypes.byref(pr)), "tfn_debug_auto")
+    return ns.value, run.value, bool(pr.value)
 
 
 # ----------------------------------------------------------------- tensor helpers

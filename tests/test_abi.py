@@ -97,3 +97,26 @@ def test_oracle_and_product_share_no_code():
             for a, b in imp.findall(open(os.path.join(ROOT, "oracle", f)).read()):
                 t = a or b
                 assert "paper_2005" not in t and "tfn_" not in t and "tfn_scenes" not in t, (f, t)
+
+
+def test_auto_state_machine_host_logic(so):
+    """AUTO (tfn_abi.cu) without a device: fast -> masked -> general above 20 % of probed row
+    steps needing the special path, back below 10 %; probe schedule: fast / masked count every
+    8th call, masked re-probes fast every 256th call, general re-probes masked every 32nd;
+    nothing is probed (or re-probed) when no read-back is possible (CUDA-graph capture)."""
+    from paper_2005_08165_b200 import tfn as T
+    nxt = lambda st, pv, r: T.tfn_debug_auto(st, pv, r, 1, False)[0]  # noqa: E731
+    # transitions after a fast probe
+    assert nxt(0, 0, 0.5) == 1 and nxt(0, 0, 0.15) == 0 and nxt(0, 0, 0.01) == 0
+    assert nxt(1, 0, 0.5) == 1 and nxt(1, 0, 0.05) == 0 and nxt(2, 0, 0.05) == 0 and nxt(2, 0, 0.5) == 2
+    # transitions after a masked probe
+    assert nxt(1, 1, 0.5) == 2 and nxt(1, 1, 0.05) == 1 and nxt(1, 1, 0.15) == 1
+    assert nxt(2, 1, 0.05) == 1 and nxt(2, 1, 0.15) == 2 and nxt(2, 1, 0.5) == 2
+    pick = lambda st, n, cp=True: T.tfn_debug_auto(st, 0, 0.0, n, cp)[1:]  # noqa: E731
+    assert pick(0, 0) == (0, True) and pick(0, 3) == (0, False) and pick(0, 8) == (0, True)
+    assert pick(0, 8, False) == (0, False)
+    assert pick(1, 256) == (0, True) and pick(1, 8) == (1, True) and pick(1, 5) == (1, False)
+    assert pick(1, 256, False) == (1, False)                  # capture: no re-probe
+    assert pick(2, 32) == (1, True) and pick(2, 8) == (2, False) and pick(2, 32, False) == (2, False)
+    with pytest.raises(T.TfnError):
+        T.tfn_debug_auto(3, 0, 0.0, 0, True)
