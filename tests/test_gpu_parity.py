@@ -380,10 +380,13 @@ def _general_cases(cfg1, random8):
     small = ts.render(ts.random_scenes(2, K33, 33, 132, seed=3), K33, 33, 132).depth.numpy()
     small[rng.random(small.shape) < 0.05] = 0.0
     d = ts.depth_to_disparity(random8.depth64[:2], 500.0, 0.12).numpy()
+    # disparity with holes and dropout (Z = 0 -> d = 0, invalid) on a ragged-width crop
+    dh = np.where(holes[:, :540, :964] > 0, (1000.0 * 0.12) / np.maximum(holes[:, :540, :964], 1e-30), 0.0)
+    dh = dh.astype(np.float32)
     return [("cfg1", cfg1.depth.numpy(), ts.K_VGA, False), ("invalid", z8, ts.K_VGA, False),
             ("quantized", q, ts.K_VGA, False), ("holes1080", holes, ts.K_1080, False),
             ("flat", flat, ts.K_VGA, False), ("small", small, K33, False),
-            ("disparity", d, ts.K_VGA, True)]
+            ("disparity", d, ts.K_VGA, True), ("disparity_holes", dh, ts.K_1080, True)]
 
 
 def test_general_kernel_bitwise_vs_pixel(tfn, cfg1, random8):
