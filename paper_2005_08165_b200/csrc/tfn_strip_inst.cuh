@@ -34,8 +34,12 @@ template <int F, int MODE>
 static cudaError_t launch_m(const KernelArgs& a, bool disp, int variant, int grid, cudaStream_t st) {
     if (a.in_u16) {
         if (disp) return cudaErrorInvalidValue;
-        return a.pts ? launch_l<F, MODE, false, 1, unsigned short, true>(a, grid, st)
-                     : launch_l<F, MODE, false, 1, unsigned short>(a, grid, st);
+        if (a.pts) return launch_l<F, MODE, false, 1, unsigned short, true>(a, grid, st);
+        // the normal encoding at compile time (N1's uint16 -> half workload is ALU-bound:
+        // no per-store run-time encoding branch)
+        return a.out_kind == 1 ? launch_l<F, MODE, false, 1, unsigned short, false, 1>(a, grid, st)
+             : a.out_kind == 2 ? launch_l<F, MODE, false, 1, unsigned short, false, 3>(a, grid, st)
+                               : launch_l<F, MODE, false, 1, unsigned short, false, 0>(a, grid, st);
     }
     if (a.pts)
         return disp ? launch_l<F, MODE, true, 1, float, true>(a, grid, st)
