@@ -84,6 +84,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/stats)")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--holes", type=int, default=None, choices=[0, 1], help="override the config's holes/salt")
     return ap.parse_args()
 
 
@@ -310,6 +311,9 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.frames:
         cfg["frames"] = args.frames
+    if args.holes is not None:
+        cfg["holes"] = bool(args.holes)
+        cfg["desc"] += " [holes overridden: %s]" % ("on" if args.holes else "off")
     ws, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, cfg, ws, rank)

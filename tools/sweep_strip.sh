@@ -8,7 +8,7 @@ for rep in 1 2; do
 import json,sys
 for l in sys.stdin:
     if l.startswith('{'):
-        d=json.loads(l); print('strip_h=$sh', round(d['value']), round(d['roofline']['frac'],4), d['clocks']['sm_mhz'], d['clocks']['reasons'])
+        d=json.loads(l); print('strip_h=$sh', round(d['value']), round(d['roofline']['frac'],4), d['clocks']['sm_mhz'], d['clocks']['reasons'], d['config'].get('kernel_variant'))
 "
   done
 done
