@@ -84,6 +84,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/stats)")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--hw", default=None, help="override the config's frame size 'H,W' (diagnostic sweeps)")
     ap.add_argument("--holes", type=int, default=None, choices=[0, 1], help="override the config's holes/salt")
     return ap.parse_args()
 
@@ -311,6 +312,10 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.frames:
         cfg["frames"] = args.frames
+    if args.hw:
+        cfg["H"], cfg["W"] = (int(x) for x in args.hw.split(","))
+        cfg["K"] = ts.K_2160 if cfg["H"] >= 2160 else ts.K_1080 if cfg["H"] >= 720 else ts.K_VGA
+        cfg["desc"] += " [frame size overridden: %dx%d]" % (cfg["H"], cfg["W"])
     if args.holes is not None:
         cfg["holes"] = bool(args.holes)
         cfg["desc"] += " [holes overridden: %s]" % ("on" if args.holes else "off")

@@ -220,15 +220,16 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
         const long long sx_n = (W + TFN_STRIP_COLS - 1) / TFN_STRIP_COLS;
         if (sh <= 0) {
             // 48 rows per strip (a multiple of the 3-row unroll; measured best on config 2 with
-            // dynamic scheduling: 12 -> 192.7, 24 -> 201.1, 48 -> 203.3 Gpx/s); halved while
-            // the batch is too small to give every resident warp two strips
-            // Wide frames take 24: on 1080x1920 (r01h sweep, 2 reps each) 12/18/24/30/36/48 ->
-            // 192.1/198.2/198.9/198.9/197.3/191.5 Gpx/s masked on configs[3], fast on the same
-            // frames without holes 24 -> 206.2 vs 48 -> 199.3, while 480x640 keeps 48 (24 -> 213.9,
-            // 48 -> 216.7 fast; 207.0 vs 210.4 masked) — a property of the width, not of the holes.
-            // The general variant keeps 48 there (166.6 at 24 vs 167.9 at 48 on configs[3]).
-            sh = (W >= 1280 && gen != 1) ? 24 : 48;
-            while (sh > 6 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 2 * resident_warps) sh /= 2;
+            // dynamic scheduling: 12 -> 192.7, 24 -> 201.1, 48 -> 203.3 Gpx/s) when it divides H;
+            // 24 when it does not (fast and masked variants).  r01h sweep (bench --strip-h, --hw,
+            // 2 reps): 1080x1920 x128 runs 198.9 at 24 vs 191.5 at 48 masked, 206.2 vs 199.3 fast
+            // (with or without holes), while 2160x3840 x32 (45 bands of 48) keeps 48: 216.9 vs 213.5
+            // fast, 210.3 vs 207.0 masked; 480x640 keeps 48 (216.7 vs 213.9).  The general
+            // variant keeps 48 (166.6 at 24 vs 167.9 at 48 on configs[3]).  Then halved while the
+            // batch gives fewer than 3 strips per resident warp (the tail: 32 x 720x1280 frames,
+            // 2.7 strips per warp at 48, run 181.1 at 24 vs 167.5 at 48)
+            sh = (H % 48 == 0 || gen == 1) ? 48 : 24;
+            while (sh > 6 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 3 * resident_warps) sh /= 2;
         }
         a.strip_h = sh;
         a.work = nullptr;
