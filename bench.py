@@ -72,7 +72,7 @@ def parse():
     ap.add_argument("--layout", default="planar", choices=["planar", "packed"])
     ap.add_argument("--out", default=None, choices=["f32", "f16", "oct16"], help="normal encoding (default: the config's)")
     ap.add_argument("--frames", type=int, default=None, help="override frames per rank")
-    ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel", "general", "masked"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "strip", "pixel", "general", "masked", "f32", "f32masked"])
     ap.add_argument("--strip-h", type=int, default=0)
     ap.add_argument("--grid", type=int, default=0)
     ap.add_argument("--static", action="store_true", help="static strip scheduling")

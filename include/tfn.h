@@ -78,10 +78,14 @@ typedef enum {
                             /* 3 general strip kernel (same results; no special path: for holes / quantized), */
                             /* 4 masked strip kernel (same results; special path only for pixels whose taps  */
                             /*   are all valid: for depth with holes / dropout)                               */
+                            /* 5 fp32 unit-step kernel (round 2 production path: within the  */
+                            /*   parity tolerance of the others, not bit-identical), 6 its masked variant    */
     TFN_OPT_STRIP_H = 1,    /* rows per warp strip, 0 = auto (>= 4)                                        */
     TFN_OPT_GRID = 2,       /* CTAs of the strip kernel, 0 = auto (resident CTAs x SMs)                    */
     TFN_OPT_DYNAMIC = 3,    /* 1 (default): strips claimed from a per-call work counter; 0: static stride  */
-    TFN_OPT_OUT_DTYPE = 4   /* tfn_out_dtype of the normals every estimate call writes (default F32)        */
+    TFN_OPT_OUT_DTYPE = 4,  /* tfn_out_dtype of the normals every estimate call writes (default F32)        */
+    TFN_OPT_COUNT_SPECIAL = 5  /* 1: the fp32 kernel counts the pixels it sends to the exact path            */
+                               /*    (read back with tfn_debug_special_count); 0 (default): not counted     */
 } tfn_option;
 
 /* Pinhole intrinsics in pixels (Eq. 13): u = column, v = row, 0-based, pixel
@@ -222,6 +226,11 @@ int tfn_auto_variant(tfn_handle h, int* variant);
  * TFN_ERR_INVALID_ARGUMENT for NULL outputs or states / variants out of range. */
 int tfn_debug_auto(int state, int probed, double rate, unsigned call, int can_probe,
                    int* next_state, int* run, int* probe);
+
+/* Pixels the fp32 unit-step kernel (TFN_OPT_KERNEL 5/6) sent to the exact per-pixel path in
+ * the last launch on h made with TFN_OPT_COUNT_SPECIAL = 1 (*count = -1 if none).
+ * Synchronous (waits for that launch).  INVALID_ARGUMENT for NULLs, CUDA on a copy error. */
+int tfn_debug_special_count(tfn_handle h, long long* count);
 
 /* ABI version (major*10000 + minor*100 + patch). */
 int tfn_version(void);

@@ -14,8 +14,9 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libtfn.so")
 SOURCES = ["tfn_abi.cu", "tfn_kernels.cu", "tfn_stats.cu", "tfn_strip_fd.cu", "tfn_strip_sobel.cu",
            "tfn_strip_scharr.cu", "tfn_strip_prewitt.cu", "tfn_strip_custom.cu",
-           "tfn_planefit.cu"]
-HEADERS = ["tfn_device.cuh", "tfn_kernels.h", "tfn_strip.cuh", "tfn_strip_inst.cuh",
+           "tfn_planefit.cu", "tfn_f32_fd.cu", "tfn_f32_sobel.cu", "tfn_f32_scharr.cu", "tfn_f32_prewitt.cu",
+           "tfn_f32_custom.cu"]
+HEADERS = ["tfn_device.cuh", "tfn_kernels.h", "tfn_strip.cuh", "tfn_strip_inst.cuh", "tfn_f32.cuh", "tfn_f32_inst.cuh",
            os.path.join("..", "..", "include", "tfn.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-fvisibility=hidden",
@@ -55,7 +56,7 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
             raise RuntimeError(f"nvcc failed for {src}")
     with open(os.path.join(HERE, "build", "ptxas.log"), "w") as f:
         f.write("\n".join(log))
-    cmd = [nvcc, *ARCH, "-shared", "-o", SO_ + ".tmp", *objs, "-lcudart"]
+    cmd = [nvcc, *ARCH, "-shared", "-o", SO_ + ".tmp", *objs, "-lcudart"]   # driver API via cudaGetDriverEntryPoint
     subprocess.check_call(cmd)
     os.replace(SO_ + ".tmp", SO_)
     if verbose:

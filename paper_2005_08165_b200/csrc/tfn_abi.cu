@@ -7,6 +7,7 @@
 #include <mutex>
 #include <new>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "../../include/tfn.h"
@@ -45,6 +46,9 @@ struct tfn_ctx {
     int sms = 148;
     int strip_ctas_per_sm[3][2] = {{0, 0}, {0, 0}, {0, 0}};   // fp32 input: [fast, general, masked][depth, disparity]
     int strip_ctas_u16 = 0;                           // uint16 depth codes (general variant)
+    int f32_ctas[2][2] = {{0, 0}, {0, 0}};            // fp32 unit-step kernel: [depth, disparity][fast, masked]
+    int count_special = 0;               // TFN_OPT_COUNT_SPECIAL: fp32 kernel counts its special pixels
+    int* last_fired = nullptr;           //   (device counter of the last such launch)
     std::mutex ws_mu;
     Workspace ws;
     int* work = nullptr;                 // ring of per-call {work, fired} counter pairs
@@ -135,6 +139,59 @@ size_t in_bytes(int in_u16) { return in_u16 ? 2 : 4; }
 size_t out_px_bytes(const tfn_ctx* h) { return h->out_kind == 0 ? 12 : h->out_kind == 1 ? 6 : 4; }
 uintptr_t out_align(const tfn_ctx* h) { return h->out_kind == 0 ? 15 : h->out_kind == 1 ? 7 : 15; }
 
+// ---- fp32 unit-step kernel (tfn_f32.cuh): TMA descriptor and guard constants ----------------
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiled encode_tiled() {
+    static EncodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiled>(p);
+        cudaGetLastError();
+    });
+    return fn;
+}
+// the input [B,H,W] fp32 as a 3-D tensor (W, H, B); boxes of 136 columns x RC rows, zero fill
+// outside (= invalid samples, Q3)
+bool f32_tensor_map(CUtensorMap* tm, const void* in, int B, int H, int W) {
+    EncodeTiled enc = encode_tiled();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
+    const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)H * W * 4};
+    const cuuint32_t box[3] = {136, TFN_F32_RC, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(in), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// with u = 2^-24, a multiplier whose three terms share one sign is accurate to
+// c1 (depth 16u incl. margin, disparity 6u); the pixel's angular error is then at most
+//   (c1 + 2u)(2 + |a|/fx + |b|/fy) + 4u + sqrt(3) u + 6u (1/fx + 1/fy) + (c1 + 14u) V/|n'|
+// and the orientation is certain when |Phi| >= 2 (c1 + 12u) V + 12u (1/fx + 1/fy) |n'|.
+// Budget: 0.8e-3 deg (the parity gate is 1e-3 deg).  Returns false when even V <= 1.5 |n'| cannot
+// be certified (tiny focal lengths): the fp32 kernel is not used then.
+bool f32_consts(const tfn_ctx* h, bool disp, tfn::F32Consts* k) {
+    const double u = std::ldexp(1.0, -24);
+    const double c1 = disp ? 6 * u : 16 * u, Ac = c1 + 2 * u, B = c1 + 14 * u;
+    const double fx = h->K.fx, fy = h->K.fy;
+    const double teff = 0.8e-3 * 3.14159265358979323846 / 180.0;
+    const double inv = 1.0 / fx + 1.0 / fy;
+    const double k0lim = (teff - 4 * u - std::sqrt(3.0) * u - 6 * u * inv - 2 * Ac) / B;
+    k->kp = (float)h->kp;
+    k->k0 = (float)h->k0;
+    k->k0lim = (float)(k0lim * (1 - 1e-6));
+    k->kca = (float)(Ac / (fx * B) * (1 + 1e-6));
+    k->kr = (float)(Ac / (fy * B) * (1 + 1e-6));
+    k->cg = (float)(12 * u * inv * (1 + 1e-6));
+    k->tb = (float)(2 * (c1 + 12 * u) * (1 + 1e-6));
+    return k0lim >= 1.5;
+}
+
 int validate(tfn_handle h, const void* in, int in_u16, int batch, int H, int W, const void* out) {
     if (!h) return TFN_ERR_INVALID_ARGUMENT;
     if (batch < 0 || H <= 0 || W <= 0) return TFN_ERR_INVALID_ARGUMENT;
@@ -182,6 +239,48 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) { cudaGetLastError(); cap = cudaStreamCaptureStatusNone; }
     const bool capturing = cap != cudaStreamCaptureStatusNone;
+    // the fp32 unit-step kernel: fp32 in / fp32 normals, no points, frames below 65536 x 65536
+    // (special-pixel queue entries pack v and u in 16 bits each), a certifiable guard
+    tfn::F32Consts f32k;
+    const bool f32_ok = strip_ok && !in_u16 && !pts && h->out_kind == 0 && H < 65536 && W < 65536 &&
+                        f32_consts(h, disp, &f32k);
+    // (not picked by AUTO: measured slower than the strip kernel on configs[1])
+    if ((kernel == tfn::TFN_KERNEL_F32 || kernel == tfn::TFN_KERNEL_F32_MASKED) && !f32_ok)
+        kernel = strip_ok ? tfn::TFN_KERNEL_STRIP : tfn::TFN_KERNEL_PIXEL;
+    if (kernel == tfn::TFN_KERNEL_F32 || kernel == tfn::TFN_KERNEL_F32_MASKED) {
+        const bool vm = kernel == tfn::TFN_KERNEL_F32_MASKED;
+        CUtensorMap tm;
+        if (!f32_tensor_map(&tm, in, batch, H, W)) return TFN_ERR_CUDA;
+        const int ctas_sm = h->f32_ctas[disp][vm];
+        const long long resident_warps = (long long)h->sms * ctas_sm * (TFN_F32_THREADS / 32);
+        const long long sx_n = (W + 127) / 128;
+        int sh = h->strip_h;
+        if (sh <= 0) {
+            sh = (H % 48 == 0) ? 48 : 24;
+            while (sh > 6 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 3 * resident_warps) sh /= 2;
+        }
+        const long long items = sx_n * ((H + sh - 1) / sh) * (long long)batch;
+        if (items >= (1LL << 31)) return TFN_ERR_INVALID_ARGUMENT;
+        a.strip_h = sh;
+        a.work = nullptr;
+        a.fired = nullptr;
+        long long ctas = h->grid > 0 ? h->grid : (long long)h->sms * ctas_sm;
+        const long long need = (items + (TFN_F32_THREADS / 32) - 1) / (TFN_F32_THREADS / 32);
+        if (ctas > need) ctas = need;
+        if (ctas < 1) ctas = 1;
+        const bool dyn = h->dynamic && items > ctas * (TFN_F32_THREADS / 32);
+        if (h->work && (dyn || h->count_special)) {
+            int* ctr = h->work + 2 * (h->call_seq.fetch_add(1) % TFN_WORK_RING);
+            if (cudaMemsetAsync(ctr, 0, 2 * sizeof(int), st) != cudaSuccess) return TFN_ERR_CUDA;
+            a.work = dyn ? ctr : nullptr;
+            a.fired = h->count_special ? ctr + 1 : nullptr;     // special pixels of this launch
+            h->last_fired = a.fired;
+        }
+        if (tfn::launch_f32_any(tm, a, f32k, h->filter, h->mode, disp, vm, (int)ctas, st) != cudaSuccess)
+            return TFN_ERR_CUDA;
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return TFN_OK;
+    }
     if (kernel == tfn::TFN_KERNEL_AUTO) {
         if (!strip_ok) {
             kernel = tfn::TFN_KERNEL_PIXEL;
@@ -294,6 +393,12 @@ TFN_API int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_han
             n = tfn::strip_occupancy(filter, nz_mode, d != 0, g, 0);
             if (n <= 0) n = 1;
         }
+    for (int d = 0; d < 2; ++d)
+        for (int m = 0; m < 2; ++m) {
+            int& n = h->f32_ctas[d][m];
+            n = tfn::f32_occupancy(filter, nz_mode, d != 0, m != 0);
+            if (n <= 0) n = 1;
+        }
     h->strip_ctas_u16 = tfn::strip_occupancy(filter, nz_mode, false, 1, 1);
     if (h->strip_ctas_u16 <= 0) h->strip_ctas_u16 = 1;
     if (cudaMalloc(&h->work, 2 * TFN_WORK_RING * sizeof(int)) != cudaSuccess) {
@@ -328,7 +433,7 @@ TFN_API int tfn_set_option(tfn_handle h, int option, long long value) {
     if (!h) return TFN_ERR_INVALID_ARGUMENT;
     switch (option) {
     case TFN_OPT_KERNEL:
-        if (value < 0 || value > 4) return TFN_ERR_INVALID_ARGUMENT;
+        if (value < 0 || value > 6) return TFN_ERR_INVALID_ARGUMENT;
         h->kernel = (int)value;
         return TFN_OK;
     case TFN_OPT_STRIP_H:
@@ -341,6 +446,9 @@ TFN_API int tfn_set_option(tfn_handle h, int option, long long value) {
         return TFN_OK;
     case TFN_OPT_DYNAMIC:
         h->dynamic = value ? 1 : 0;
+        return TFN_OK;
+    case TFN_OPT_COUNT_SPECIAL:
+        h->count_special = value ? 1 : 0;
         return TFN_OK;
     case TFN_OPT_OUT_DTYPE:
         if (value != TFN_OUT_F32 && value != TFN_OUT_F16 && value != TFN_OUT_OCT16) return TFN_ERR_INVALID_ARGUMENT;
@@ -583,4 +691,14 @@ TFN_API int tfn_debug_auto(int state, int probed, double rate, unsigned call, in
     return TFN_OK;
 }
 
-TFN_API int tfn_version(void) { return 100; }
+TFN_API int tfn_debug_special_count(tfn_handle h, long long* count) {
+    if (!h || !count) return TFN_ERR_INVALID_ARGUMENT;
+    *count = -1;
+    if (!h->last_fired) return TFN_OK;
+    int n = 0;
+    if (cudaMemcpy(&n, h->last_fired, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return TFN_ERR_CUDA;
+    *count = n;
+    return TFN_OK;
+}
+
+TFN_API int tfn_version(void) { return 200; }

@@ -1,0 +1,3 @@
+// tfn_f32_scharr.cu — fp32 unit-step kernel instantiations for the scharr filter (see tfn_f32_inst.cuh).
+#include "tfn_f32_inst.cuh"
+TFN_INSTANTIATE_F32(tfn::SCHARR)

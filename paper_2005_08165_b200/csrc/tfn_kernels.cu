@@ -100,6 +100,27 @@ int strip_occupancy(int filter, int mode, bool disp, int variant, int in_u16) {
     }
 }
 
+cudaError_t launch_f32_any(const CUtensorMap& tm, const KernelArgs& a, const F32Consts& k, int filter, int mode,
+                           bool disp, bool vm, int grid, cudaStream_t st) {
+    switch (filter) {
+    case FD: return launch_f32<FD>(tm, a, k, mode, disp, vm, grid, st);
+    case SOBEL: return launch_f32<SOBEL>(tm, a, k, mode, disp, vm, grid, st);
+    case SCHARR: return launch_f32<SCHARR>(tm, a, k, mode, disp, vm, grid, st);
+    case PREWITT: return launch_f32<PREWITT>(tm, a, k, mode, disp, vm, grid, st);
+    default: return launch_f32<CUSTOM>(tm, a, k, mode, disp, vm, grid, st);
+    }
+}
+
+int f32_occupancy(int filter, int mode, bool disp, bool vm) {
+    switch (filter) {
+    case FD: return occupancy_f32<FD>(mode, disp, vm);
+    case SOBEL: return occupancy_f32<SOBEL>(mode, disp, vm);
+    case SCHARR: return occupancy_f32<SCHARR>(mode, disp, vm);
+    case PREWITT: return occupancy_f32<PREWITT>(mode, disp, vm);
+    default: return occupancy_f32<CUSTOM>(mode, disp, vm);
+    }
+}
+
 cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, int kernel,
                         int grid_strip, cudaStream_t st) {
     switch (filter) {

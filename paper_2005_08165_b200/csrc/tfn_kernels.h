@@ -2,6 +2,7 @@
 // kernels (tfn_kernels.cu + tfn_strip_<filter>.cu, tfn_stats.cu).  Not part of the public
 // ABI (include/tfn.h).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #ifndef TFN_STRIP_THREADS
@@ -14,11 +15,17 @@
 #define TFN_STRIP_PPL 4          // strip kernel: pixels (columns) per lane
 #endif
 #define TFN_STRIP_COLS (32 * TFN_STRIP_PPL)   // columns per warp strip
+#ifndef TFN_F32_THREADS
+#define TFN_F32_THREADS 128      // fp32 unit-step kernel: threads per CTA
+#endif
+#ifndef TFN_F32_RC
+#define TFN_F32_RC 4             //   rows per TMA box
+#endif
 
 namespace tfn {
 
 enum KernelId { TFN_KERNEL_AUTO = 0, TFN_KERNEL_PIXEL = 1, TFN_KERNEL_STRIP = 2, TFN_KERNEL_STRIP_GENERAL = 3,
-                TFN_KERNEL_STRIP_MASKED = 4 };
+                TFN_KERNEL_STRIP_MASKED = 4, TFN_KERNEL_F32 = 5, TFN_KERNEL_F32_MASKED = 6 };
 
 enum InDtype { TFN_IN_F32 = 0, TFN_IN_U16 = 1 };
 
@@ -41,6 +48,22 @@ struct KernelArgs {
     float ifx, ify;      //   1/fx, 1/fy
     double kp, k0;       // CUSTOM filter weights [kp k0 kp] (ignored by the fixed filters)
 };
+
+// fp32 unit-step kernel (tfn_f32.cuh): guard constants computed on the host
+struct F32Consts {
+    float kp, k0;          // CUSTOM weights (fp32)
+    float k0lim, kca, kr;  // guard: V <= (k0lim - kca |a| - kr |b|) |n'|
+    float cg, tb;          //   and |Phi| >= cg |n'| + tb V (the orientation is certain)
+};
+namespace f32 { using Consts = F32Consts; }
+template <int F>
+cudaError_t launch_f32(const CUtensorMap& tm, const KernelArgs& a, const F32Consts& k, int mode, bool disp, bool vm,
+                       int grid, cudaStream_t st);
+template <int F>
+int occupancy_f32(int mode, bool disp, bool vm);
+cudaError_t launch_f32_any(const CUtensorMap& tm, const KernelArgs& a, const F32Consts& k, int filter, int mode,
+                           bool disp, bool vm, int grid, cudaStream_t st);
+int f32_occupancy(int filter, int mode, bool disp, bool vm);
 
 cudaError_t launch_3f2n(const KernelArgs& a, int filter, int mode, bool disp, int kernel,
                         int grid_strip, cudaStream_t st);

@@ -24,9 +24,9 @@ TFN_OK, TFN_ERR_INVALID_ARGUMENT, TFN_ERR_CONFIG, TFN_ERR_CUDA = 0, 1, 2, 3
 FILTERS = {"fd": 0, "sobel": 1, "scharr": 2, "prewitt": 3, "custom": 4}
 MODES = {"mean": 0, "median": 1}
 LAYOUTS = {"planar": 0, "packed": 1}
-KERNELS = {"auto": 0, "pixel": 1, "strip": 2, "general": 3, "masked": 4}
+KERNELS = {"auto": 0, "pixel": 1, "strip": 2, "general": 3, "masked": 4, "f32": 5, "f32masked": 6}
 OUT_DTYPES = {"f32": 0, "f16": 1, "oct16": 2}
-OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_DYNAMIC, OPT_OUT_DTYPE = 0, 1, 2, 3, 4
+OPT_KERNEL, OPT_STRIP_H, OPT_GRID, OPT_DYNAMIC, OPT_OUT_DTYPE, OPT_COUNT_SPECIAL = 0, 1, 2, 3, 4, 5
 
 # every symbol include/tfn.h declares (tests/test_abi.py checks the export table)
 ABI_SYMBOLS = (
@@ -34,7 +34,7 @@ ABI_SYMBOLS = (
     "tfn_estimate_host", "tfn_stats", "tfn_debug_phi8", "tfn_destroy", "tfn_status_string",
     "tfn_kernel_launches", "tfn_version", "tfn_debug_sol", "tfn_auto_variant", "tfn_estimate_u16",
     "tfn_estimate_host_u16", "tfn_estimate_points", "tfn_set_filter_weights", "tfn_plane_fit",
-    "tfn_debug_auto",
+    "tfn_debug_auto", "tfn_debug_special_count",
 )
 PLANE_METHODS = {"pca": 0, "svd": 1}
 INPUT_KINDS = {"depth": 0, "disparity": 1, "depth_u16": 2}
@@ -81,6 +81,7 @@ def lib() -> ctypes.CDLL:
         L.tfn_auto_variant.argtypes = [vp, ctypes.POINTER(i)]
         L.tfn_debug_auto.argtypes = [i, i, d, ctypes.c_uint, i, ctypes.POINTER(i), ctypes.POINTER(i),
                                      ctypes.POINTER(i)]
+        L.tfn_debug_special_count.argtypes = [vp, ctypes.POINTER(ll)]
         L.tfn_status_string.argtypes = [i]
         L.tfn_status_string.restype = ctypes.c_char_p
         L.tfn_kernel_launches.restype = ctypes.c_ulonglong
@@ -93,13 +94,19 @@ def lib() -> ctypes.CDLL:
                                                      "tfn_auto_variant", "tfn_estimate_u16",
                                                      "tfn_estimate_host_u16", "tfn_estimate_points",
                                                      "tfn_set_filter_weights", "tfn_plane_fit",
-                                                     "tfn_debug_auto"):
+                                                     "tfn_debug_auto", "tfn_debug_special_count"):
                 f.restype = ctypes.c_int
         _lib = L
     return _lib
 
 
 # ----------------------------------------------------------------- ABI-named calls
+def tfn_debug_special_count(h: int) -> int:
+    n = ctypes.c_longlong()
+    _check(lib().tfn_debug_special_count(h, ctypes.byref(n)), "tfn_debug_special_count")
+    return n.value
+
+
 def tfn_status_string(status: int) -> str:
     try:
         return lib().tfn_status_string(int(status)).decode()
