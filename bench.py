@@ -11,8 +11,10 @@ Inputs (1.26 GB) exceed the 126 MB L2, so no flush is needed between steps.
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the fp64 CPU oracle
 (oracle/, the only non-test code allowed to run it) on the same config/metric.
-Multi-GPU: torchrun; per-rank timing with CUDA events, max over ranks; NCCL only
-all-reduces the int64 angular-error statistics (off the timed region).
+Multi-GPU: `--gpus N` re-launches itself under torch.distributed.run with N ranks (one per
+GPU) unless it already runs under torchrun (WORLD_SIZE set); per-rank timing with CUDA
+events, max over ranks; NCCL only all-reduces the int64 angular-error statistics (off the
+timed region).  `--dry-run` exercises the same rank logic on CPU with gloo (tests).
 """
 from __future__ import annotations
 
@@ -86,10 +88,83 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--hw", default=None, help="override the config's frame size 'H,W' (diagnostic sweeps)")
     ap.add_argument("--holes", type=int, default=None, choices=[0, 1], help="override the config's holes/salt")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo rehearsal of the multi-rank logic (frame shards, barriers, max-over-ranks "
+                         "timing, one JSON line); no GPU, no kernel")
     return ap.parse_args()
 
 
 # ------------------------------------------------------------------ helpers
+def relaunch(args) -> int:
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run with N ranks on
+    this node (rendezvous on 127.0.0.1, a free port) and return its exit code."""
+    import socket
+    import subprocess
+    if not args.dry_run and args.impl != "reference":
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def rank_frames(cfg, rank, ws):
+    """Global frame range [first, last) of this rank: config 5 shards a fixed total over the
+    ranks (strong scaling); every other config gives each rank its own full batch (weak)."""
+    from paper_2005_08165_b200 import dist as tdist
+    if cfg.get("stream", False):
+        return tdist.shard(cfg["frames"], rank, ws)
+    return rank * cfg["frames"], (rank + 1) * cfg["frames"]
+
+
+def run_dry(args, cfg, ws, rank):
+    """The multi-rank plumbing of the GPU arm on CPU (gloo): init, frame shards, start barrier,
+    a per-rank 'step' (CPU work proportional to the shard), end barrier, max-over-ranks timing
+    (all-reduce MAX), the int64 stats all-reduce, and rank 0's JSON line.  No kernel runs: the
+    value is not a measurement (tests/test_bench_contract.py checks the logic only)."""
+    import torch.distributed as dist
+    if ws > 1:
+        dist.init_process_group("gloo")
+    first, last = rank_frames(cfg, rank, ws)
+    per_rank = last - first
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    acc = torch.zeros(8, dtype=torch.int64)
+    for _ in range(max(1, args.steps)):
+        acc[7] += per_rank * cfg["H"] * cfg["W"]           # pixels "processed" (n_pixels slot)
+    dt = torch.tensor([time.perf_counter() - t0 + 1e-6], dtype=torch.float64)
+    if ws > 1:
+        dist.barrier()
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM)
+        ranges = [None] * ws
+        dist.all_gather_object(ranges, (first, last))
+    else:
+        ranges = [(first, last)]
+    if rank == 0:
+        units = acc[7].item()
+        line = {"metric": METRIC, "value": units / dt.item() / 1e6, "unit": "Mpixel/s", "n_gpus": ws,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt.item() * 1e3 / max(1, args.steps),
+                "higher_is_better": True, "scaling": "strong" if cfg.get("stream") else "weak", "vs_baseline": None,
+                "dtype": "none (dry run)", "data": "none (dry run: rank logic only, no kernel)", "dry_run": True,
+                "config": {"workload": cfg["desc"], "frames_per_gpu": per_rank, "H": cfg["H"], "W": cfg["W"],
+                           "rank_frames": [list(r) for r in ranges],
+                           "parallelism": f"dp{ws} (frame batches sharded, no collective on the hot path)"},
+                "gpu_launches": 0}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -320,6 +395,12 @@ def main():
         cfg["holes"] = bool(args.holes)
         cfg["desc"] += " [holes overridden: %s]" % ("on" if args.holes else "off")
     ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    if ws != args.gpus and rank == 0:
+        print(f"bench.py: running {ws} rank(s) as launched (--gpus {args.gpus})", file=sys.stderr)
+    if args.dry_run:
+        return run_dry(args, cfg, ws, rank)
     if args.impl == "reference":
         return run_reference(args, cfg, ws, rank)
 
@@ -336,10 +417,7 @@ def main():
     H, W, K = cfg["H"], cfg["W"], cfg["K"]
     from paper_2005_08165_b200 import dist as tdist
     streaming_cfg = cfg.get("stream", False)
-    if streaming_cfg:          # config 5: a fixed total, sharded by frame over the ranks
-        first, last = tdist.shard(cfg["frames"], rank, ws)
-    else:                      # weak scaling: every rank renders its own batch
-        first, last = rank * cfg["frames"], (rank + 1) * cfg["frames"]
+    first, last = rank_frames(cfg, rank, ws)       # config 5: a fixed total sharded; else weak scaling
     per_rank = last - first
     chunk = min(per_rank, 1024) if streaming_cfg else per_rank
 

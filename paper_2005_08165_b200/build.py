@@ -16,7 +16,7 @@ SOURCES = ["tfn_abi.cu", "tfn_kernels.cu", "tfn_stats.cu", "tfn_strip_fd.cu", "t
            "tfn_strip_scharr.cu", "tfn_strip_prewitt.cu", "tfn_strip_custom.cu",
            "tfn_planefit.cu", "tfn_f32_fd.cu", "tfn_f32_sobel.cu", "tfn_f32_scharr.cu", "tfn_f32_prewitt.cu",
            "tfn_f32_custom.cu"]
-HEADERS = ["tfn_device.cuh", "tfn_kernels.h", "tfn_strip.cuh", "tfn_strip_inst.cuh", "tfn_f32.cuh", "tfn_f32_inst.cuh",
+HEADERS = ["tfn_device.cuh", "tfn_kernels.h", "tfn_strip.cuh", "tfn_strip_inst.cuh", "tfn_f32.cuh", "tfn_f32_inst.cuh", "tfn_tma.cuh",
            os.path.join("..", "..", "include", "tfn.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-fvisibility=hidden",

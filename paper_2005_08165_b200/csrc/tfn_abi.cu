@@ -12,6 +12,9 @@
 
 #include "../../include/tfn.h"
 #include "tfn_kernels.h"
+#ifndef TFN_STRIP_TMA
+#define TFN_STRIP_TMA 1
+#endif
 
 #define TFN_API extern "C" __attribute__((visibility("default")))
 
@@ -53,6 +56,7 @@ struct tfn_ctx {
     Workspace ws;
     int* work = nullptr;                 // ring of per-call {work, fired} counter pairs
     std::atomic<unsigned> call_seq{0};
+    std::atomic<unsigned> capture_seq{0};    // next dedicated capture slot (after the ring)
     // AUTO kernel selection: the fast and masked strip variants count their special row
     // steps; the count comes back through a pinned word a few calls later and moves the
     // choice fast -> masked -> general (and back)
@@ -66,6 +70,7 @@ struct tfn_ctx {
     unsigned auto_calls = 0;
 };
 #define TFN_WORK_RING 4096
+#define TFN_CAPTURE_SLOTS 1024           // counter pairs reserved for CUDA-graph captures (never reused)
 // AUTO: step to the next variant (fast -> masked -> general) when more than this fraction
 // of the probed variant's row steps needed the special path (measured break-even ~0.24:
 // config 2 has 0.011 and runs 217 fast vs 210 masked vs 167 general; config 4 (holes + 1 %
@@ -163,7 +168,7 @@ bool f32_tensor_map(CUtensorMap* tm, const void* in, int B, int H, int W) {
     if (!enc) return false;
     const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)B};
     const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)H * W * 4};
-    const cuuint32_t box[3] = {136, TFN_F32_RC, 1};
+    const cuuint32_t box[3] = {(cuuint32_t)tfn::ring::BOXW, (cuuint32_t)tfn::ring::RC, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(in), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -192,6 +197,21 @@ bool f32_consts(const tfn_ctx* h, bool disp, tfn::F32Consts* k) {
     return k0lim >= 1.5;
 }
 
+// The {work, fired} counter pair a launch uses.  Direct calls take the next pair of a ring of
+// TFN_WORK_RING (zeroed by a memset on the launch's stream just before the kernel).  A launch
+// being captured into a CUDA graph gets a pair of its own that no other launch ever uses: the
+// graph's memset node re-zeroes it at every replay, so a replay can run concurrently with any
+// direct call (a ring slot baked into a graph was handed out again 4096 calls
+// later).  When the capture pairs run out, captured launches schedule strips statically
+// (no counter; same results).  nullptr: no counter available.
+int* counter_pair(tfn_ctx* h, bool capturing) {
+    if (!h->work) return nullptr;
+    if (!capturing) return h->work + 2 * (h->call_seq.fetch_add(1) % TFN_WORK_RING);
+    const unsigned k = h->capture_seq.fetch_add(1);
+    if (k >= TFN_CAPTURE_SLOTS) return nullptr;
+    return h->work + 2 * (TFN_WORK_RING + k);
+}
+
 int validate(tfn_handle h, const void* in, int in_u16, int batch, int H, int W, const void* out) {
     if (!h) return TFN_ERR_INVALID_ARGUMENT;
     if (batch < 0 || H <= 0 || W <= 0) return TFN_ERR_INVALID_ARGUMENT;
@@ -208,6 +228,7 @@ int validate(tfn_handle h, const void* in, int in_u16, int batch, int H, int W, 
 int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, int W, cudaStream_t st,
         void* out, float* pts = nullptr, double pscale = 1.0) {
     tfn::KernelArgs a;
+    a.tmap = nullptr;
     a.in = in;
     a.out = out;
     a.in_u16 = in_u16;
@@ -228,7 +249,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
     a.layout = h->layout;
     // strip kernel: 4-sample vectors in and 4-component vectors out (16 B fp32, 8 B for
     // uint16 / half), and (frame, strip-row, strip-col) items indexed in 32 bits
-    const long long max_items = (long long)((W + TFN_STRIP_COLS - 1) / TFN_STRIP_COLS) * ((H + 3) / 4) * (long long)batch;
+    const long long max_items = (long long)((W + TFN_STRIP_COLS - 1) / TFN_STRIP_COLS) * (long long)batch;   // at strip_h = H
     const uintptr_t in_al = 4 * in_bytes(in_u16) - 1, out_al = out_align(h);
     const bool strip_ok = (W % 4 == 0) && (((uintptr_t)in & in_al) == 0) && (((uintptr_t)out & out_al) == 0) &&
                           (((uintptr_t)pts & 15) == 0) && max_items < (1LL << 31);
@@ -259,6 +280,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
             sh = (H % 48 == 0) ? 48 : 24;
             while (sh > 6 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 3 * resident_warps) sh /= 2;
         }
+        while (sx_n * ((H + sh - 1) / sh) * (long long)batch >= (1LL << 31) && sh < H) sh = sh * 2 < H ? sh * 2 : H;
         const long long items = sx_n * ((H + sh - 1) / sh) * (long long)batch;
         if (items >= (1LL << 31)) return TFN_ERR_INVALID_ARGUMENT;
         a.strip_h = sh;
@@ -269,8 +291,8 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
         if (ctas > need) ctas = need;
         if (ctas < 1) ctas = 1;
         const bool dyn = h->dynamic && items > ctas * (TFN_F32_THREADS / 32);
-        if (h->work && (dyn || h->count_special)) {
-            int* ctr = h->work + 2 * (h->call_seq.fetch_add(1) % TFN_WORK_RING);
+        int* ctr = (dyn || h->count_special) ? counter_pair(h, capturing) : nullptr;
+        if (ctr) {
             if (cudaMemsetAsync(ctr, 0, 2 * sizeof(int), st) != cudaSuccess) return TFN_ERR_CUDA;
             a.work = dyn ? ctr : nullptr;
             a.fired = h->count_special ? ctr + 1 : nullptr;     // special pixels of this launch
@@ -330,6 +352,9 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
             sh = (H % 48 == 0 || gen == 1) ? 48 : 24;
             while (sh > 6 && sx_n * ((H + sh - 1) / sh) * (long long)batch < 3 * resident_warps) sh /= 2;
         }
+        // (frame, strip-row, strip-col) items are indexed in 32 bits: raise a small requested
+        // strip height until they fit (results do not depend on it)
+        while (sx_n * ((H + sh - 1) / sh) * (long long)batch >= (1LL << 31) && sh < H) sh = sh * 2 < H ? sh * 2 : H;
         a.strip_h = sh;
         a.work = nullptr;
         a.fired = nullptr;
@@ -343,14 +368,22 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
         // no more items than warps it is pure overhead (a memset node per call: single
         // frames 14.5 -> 12.5 us per graph-replayed call measured)
         const bool dyn = h->dynamic && items > ctas * (TFN_STRIP_THREADS / 32);
-        if (h->work && (dyn || probe)) {
-            int* ctr = h->work + 2 * (h->call_seq.fetch_add(1) % TFN_WORK_RING);
+        int* ctr = (dyn || probe) ? counter_pair(h, capturing) : nullptr;
+        if (ctr) {
             if (cudaMemsetAsync(ctr, 0, 2 * sizeof(int), st) != cudaSuccess) return TFN_ERR_CUDA;
             a.work = dyn ? ctr : nullptr;
             a.fired = probe ? ctr + 1 : nullptr;
         }
     } else {
         a.strip_h = 0;
+    }
+    // strip kernels on fp32 input read their rows through the TMA ring (tfn_tma.cuh)
+    static const CUtensorMap zero_tm = {};
+    CUtensorMap tmv;
+    a.tmap = &zero_tm;
+    if (strip && !in_u16 && TFN_STRIP_TMA) {
+        if (!f32_tensor_map(&tmv, in, batch, H, W)) return TFN_ERR_CUDA;
+        a.tmap = &tmv;
     }
     cudaError_t e = tfn::launch_3f2n(a, h->filter, h->mode, disp, kernel, grid, st);
     if (e != cudaSuccess) return TFN_ERR_CUDA;
@@ -401,7 +434,7 @@ TFN_API int tfn_create(const tfn_intrinsics* K, int filter, int nz_mode, tfn_han
         }
     h->strip_ctas_u16 = tfn::strip_occupancy(filter, nz_mode, false, 1, 1);
     if (h->strip_ctas_u16 <= 0) h->strip_ctas_u16 = 1;
-    if (cudaMalloc(&h->work, 2 * TFN_WORK_RING * sizeof(int)) != cudaSuccess) {
+    if (cudaMalloc(&h->work, 2 * (TFN_WORK_RING + TFN_CAPTURE_SLOTS) * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         h->work = nullptr;                // static scheduling (and the fast AUTO choice) still work
     }
@@ -517,6 +550,8 @@ int host_run(tfn_handle h, const void* host_in, int in_u16, bool disp, int batch
     const size_t fpx = (size_t)H * (size_t)W;
     if ((unsigned long long)batch * fpx > (1ull << 60) / 12) return TFN_ERR_INVALID_ARGUMENT;
     const size_t fin = fpx * in_bytes(in_u16), fout = fpx * out_px_bytes(h);
+    // chunk k+1's H2D would read input that chunk k's D2H already overwrote
+    if (overlap(host_in, (size_t)batch * fin, host_out, (size_t)batch * fout)) return TFN_ERR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lock(h->ws_mu);
     Workspace& ws = h->ws;
     size_t chunk = (48u << 20) / fin;

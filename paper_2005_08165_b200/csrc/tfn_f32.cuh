@@ -43,12 +43,10 @@
 
 #include "tfn_device.cuh"
 #include "tfn_kernels.h"
+#include "tfn_tma.cuh"
 
 #ifndef TFN_F32_MINBLOCKS
 #define TFN_F32_MINBLOCKS 4
-#endif
-#ifndef TFN_F32_NS
-#define TFN_F32_NS 4             // ring slots per warp
 #endif
 
 namespace tfn {
@@ -56,17 +54,18 @@ namespace f32 {
 
 constexpr int PPL = 4;                       // pixels (columns) per lane
 constexpr int NW = PPL + 2;                  // window width (1 halo column each side)
-constexpr int RC = TFN_F32_RC;
-constexpr int NS = TFN_F32_NS;
-constexpr int BOXW = 136;                    // box columns: c0-4 .. c0+131
+using ring::RC;
+using ring::NS;
+using ring::BOXW;
 constexpr int WARPS = TFN_F32_THREADS / 32;
 constexpr int QCAP = 32 + 32 * PPL;          // special-pixel queue entries per warp
 
 struct __align__(128) Smem {
-    float ring[WARPS][NS][RC][BOXW];         // 544-B rows: 16-B aligned lane vectors
+    float ring[WARPS][NS][RC][BOXW];         // 544-B rows: 16-B aligned lane vectors (tfn_tma.cuh)
     unsigned long long bar[WARPS][NS];
     int q[WARPS][QCAP];
 };
+using ring::Ring;
 
 // ---- guard constants.  u = 2^-24; rcp.approx <= 2^-22 relative.
 //      depth: D = -(dZ w_o) w_x: 3 roundings + 2 reciprocals = 11u; sums of <= 6 terms: +6u;
@@ -388,59 +387,6 @@ __device__ __forceinline__ unsigned row_step(const Ctx& c, const Win& rm, const 
     return sp;
 }
 
-// ---- TMA ring ----------------------------------------------------------------------------------
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void bar_init(unsigned bar) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar) : "memory");
-}
-__device__ __forceinline__ void tma_row_box(const CUtensorMap* tm, unsigned dst, unsigned bar, int x, int y, int b) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(RC * BOXW * 4) : "memory");
-    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
-                 :: "r"(dst), "l"(tm), "r"(x), "r"(y), "r"(b), "r"(bar) : "memory");
-}
-__device__ __forceinline__ void bar_wait(unsigned bar, unsigned parity) {
-    unsigned done = 0;
-    do {
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-    } while (!done);
-}
-
-struct Ring {
-    unsigned base, bar;        // this warp's slots / barriers (shared addresses)
-    unsigned kq;               // chunks this warp consumed before the current strip
-    int nch;                   // chunks of the current strip
-    int x, y, b;               // box origin of chunk 0 of the current strip
-};
-
-// issue chunk k of the current strip into its slot (lane 0 only)
-__device__ __forceinline__ void ring_issue(const CUtensorMap* tm, const Ring& r, int k) {
-    const unsigned g = r.kq + (unsigned)k, slot = g % NS;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    tma_row_box(tm, r.base + slot * (RC * BOXW * 4), r.bar + slot * 8, r.x, r.y + k * RC, r.b);
-}
-
-// row rr (0 = the strip's first row - 1) of the current strip into the lane's window
-__device__ __forceinline__ void ring_row(const CUtensorMap* tm, const Ring& r, int rr, int lane, float zr[NW]) {
-    const int k = rr / RC, rw = rr - k * RC;
-    const unsigned g = r.kq + (unsigned)k, slot = g % NS;
-    if (rw == 0) {
-        // chunk k starts: chunk k-1 is consumed, its slot takes chunk k-1+NS
-        if (k > 0 && k - 1 + NS < r.nch) {
-            __syncwarp();
-            if (lane == 0) ring_issue(tm, r, k - 1 + NS);
-        }
-        bar_wait(r.bar + slot * 8, (g / NS) & 1u);
-    }
-    const unsigned a = r.base + slot * (RC * BOXW * 4) + rw * (BOXW * 4) + 16u + 16u * (unsigned)lane;
-    float4 m;
-    float hl, hr;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(m.x), "=f"(m.y), "=f"(m.z), "=f"(m.w) : "r"(a));
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(hl) : "r"(a - 4u));
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(hr) : "r"(a + 16u));
-    zr[0] = hl; zr[1] = m.x; zr[2] = m.y; zr[3] = m.z; zr[4] = m.w; zr[5] = hr;
-}
-
 // first row of a strip (row y0 - 1): its window, H, E-pair reciprocals and masks; the rest of
 // the link is only read by the priming step, whose outputs are discarded
 template <int F, bool DISP, bool VM>
@@ -528,15 +474,7 @@ tfn_f32_kernel(const __grid_constant__ CUtensorMap tm, const KernelArgs p, const
     constexpr bool CUST = (F == CUSTOM);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     Ring rg;
-    rg.base = smem_u32(&sm.ring[wid][0][0][0]);
-    rg.bar = smem_u32(&sm.bar[wid][0]);
-    rg.kq = 0;
-    if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < NS; ++k) bar_init(rg.bar + 8 * k);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
+    ring::ring_init(rg, &sm.ring[wid][0][0][0], &sm.bar[wid][0], lane);
     int* q = sm.q[wid];
     int qn = 0;
 
@@ -572,17 +510,13 @@ tfn_f32_kernel(const __grid_constant__ CUtensorMap tm, const KernelArgs p, const
         float* ofr = reinterpret_cast<float*>(p.out) + (long long)fb * 3 * HW;
         float* orow = ofr + (LAYOUT == 0 ? (long long)c0 : 3LL * c0);
 
-        // this strip's rows y0-1 .. y1 in chunks of RC
-        rg.nch = (y1 - y0 + 2 + RC - 1) / RC;
-        rg.x = sx * 128 - 4; rg.y = y0 - 1; rg.b = fb;
-        __syncwarp();
-        if (lane == 0)
-            for (int k = 0; k < NS && k < rg.nch; ++k) ring_issue(&tm, rg, k);
+        // this strip's rows y0-1 .. y1 through the TMA ring
+        ring::ring_strip(&tm, rg, sx * 128 - 4, y0, y1, fb, lane);
 
         Win win[3];
         Link lk[3];
         float zr[NW];
-        ring_row(&tm, rg, 0, lane, zr);
+        ring::ring_row(&tm, rg, 0, lane, zr);
         strip_init<F, DISP, VM>(win[0], lk[0], zr);
         win[2] = win[0];
         float ox[PPL], oy[PPL], oz[PPL];
@@ -592,7 +526,7 @@ tfn_f32_kernel(const __grid_constant__ CUtensorMap tm, const KernelArgs p, const
 #define TFN_F32_STEP(S)                                                                                        \
         {                                                                                                      \
             const int v = y0 - 1 + s;                                                                          \
-            ring_row(&tm, rg, s + 1, lane, zr);                                                                \
+            ring::ring_row(&tm, rg, s + 1, lane, zr);                                                              \
             const float bf = __fsub_rn(__int2float_rn(v), p.v0);                                               \
             unsigned sp = row_step<F, MODE, DISP, VM, CUST>(c, win[((S) + 2) % 3], win[(S) % 3], win[((S) + 1) % 3], \
                                                             lk[(S) % 3], lk[((S) + 1) % 3], zr, bf,           \
@@ -614,7 +548,7 @@ tfn_f32_kernel(const __grid_constant__ CUtensorMap tm, const KernelArgs p, const
             TFN_F32_STEP(0) TFN_F32_STEP(1) TFN_F32_STEP(2)
         }
 #undef TFN_F32_STEP
-        rg.kq += (unsigned)rg.nch;
+        ring::ring_strip_done(rg);
         if (qn > 0)
             queue_flush<F, MODE, DISP, LAYOUT>(q, qn, true, img, ofr, p.H, p.W, p.u0, p.v0, p.fx, p.fy, p.kp, p.k0, lane);
         if (p.work) {

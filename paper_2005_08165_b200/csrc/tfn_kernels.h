@@ -18,9 +18,7 @@
 #ifndef TFN_F32_THREADS
 #define TFN_F32_THREADS 128      // fp32 unit-step kernel: threads per CTA
 #endif
-#ifndef TFN_F32_RC
-#define TFN_F32_RC 4             //   rows per TMA box
-#endif
+#include "tfn_tma.cuh"
 
 namespace tfn {
 
@@ -47,6 +45,7 @@ struct KernelArgs {
     float pscale;        //   Z = pscale * sample (depth, incl. uint16 codes) or pscale / d (disparity)
     float ifx, ify;      //   1/fx, 1/fy
     double kp, k0;       // CUSTOM filter weights [kp k0 kp] (ignored by the fixed filters)
+    const CUtensorMap* tmap;   // strip kernel, fp32 input: TMA descriptor of the input (tfn_tma.cuh)
 };
 
 // fp32 unit-step kernel (tfn_f32.cuh): guard constants computed on the host

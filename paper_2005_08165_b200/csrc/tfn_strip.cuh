@@ -41,6 +41,10 @@
 #ifndef TFN_STRIP_PPL
 #define TFN_STRIP_PPL 4          // pixels (columns) per lane: 4 or 2
 #endif
+#ifndef TFN_STRIP_TMA
+#define TFN_STRIP_TMA 1          // fp32 input rows through the per-warp TMA ring (tfn_tma.cuh) instead of
+#endif                           // the three-rows-ahead register prefetch
+#include "tfn_tma.cuh"
 
 namespace tfn {
 
@@ -78,6 +82,9 @@ struct StripCtx {
     int y1;            // end row of the current strip
     unsigned ring;     // shared-memory address of this warp's row ring (uint16 input)
     int lane;
+    ring::Ring* rg;    // fp32 input with TFN_STRIP_TMA: this warp's TMA row ring
+    const CUtensorMap* tm;
+    int ys;            //   first output row of the current strip (ring row = v - ys + 1)
 };
 
 
@@ -308,6 +315,15 @@ __device__ __forceinline__ void store_packed(__half* o, const float* x, const fl
 // One row step: output row v.  P = slot(v-1) (only P.w is read; P.raw holds row v+2 in
 // flight), C = slot(v) (C.raw receives row v+3), N = slot(v+1) (N.raw loaded; the rest
 // computed here).
+// TMA row staging (tfn_tma.cuh) for fp32 input.  A/B on configs[1] (r02, 1024 x 480x640, Sobel):
+// median fast 211 (TMA) vs 218 (register prefetch), masked 211 vs 212, general 176 vs 172; mean
+// fast 261 vs 252, masked 263 vs 247, general 168 vs 177 Gpx/s — the register window already
+// loads every sample once (loads are 1/4 of the traffic), so the ring only removes the prefetch
+// registers; it stays off where it measured slower (fast median, general mean).
+template <class T, int MODE, bool GEN, bool VM>
+constexpr bool TMA_ON = (TFN_STRIP_TMA != 0) && (sizeof(T) == 4) && !(MODE == MEDIAN && !GEN && !VM) &&
+                        !(MODE == MEAN && GEN);
+
 template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT, bool VM = false>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
                                          char* __restrict__ out, long long HW,
@@ -319,6 +335,9 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         cpa_wait<TFN_CPA_D - 2>();
         __syncwarp();                                // halo words come from the neighbour lanes' copies
         fetch_row(N, c, v + 1);
+    } else if (TMA_ON<T, MODE, GEN, VM>) {
+        ring::ring_row(c.tm, *c.rg, v + 2 - c.ys, c.lane, N.raw);   // row v+1 from the TMA ring
+        N.rok = true;                                // rows outside the image arrive zero-filled
     } else {
         load_raw(C, c, v + 3);                       // prefetch three rows ahead (C.raw is free)
     }
@@ -573,7 +592,11 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
                                           unsigned colmask, int ys, int y1) {
     Slot S0, S1, S2;
     if constexpr (Ring<T, GEN>::on) {
-        // prologue: rows ys-1 .. ys+D-2 issued (one group each), rows ys-1 (S0), ys (S1) prepared
+        // prologue: rows ys-1 .. ys+D-2 issued (one group each), rows ys-1 (S0), ys (S1) prepared.
+        // The previous strip's last fetches read neighbour lanes' halo words from slots these
+        // copies may overwrite: order them (with dynamic scheduling the item shuffle
+        // already did)
+        __syncwarp();
     #pragma unroll
         for (int r = -1; r <= TFN_CPA_D - 2; ++r) {
             if (ys + r <= y1) issue_row(c, ys + r);
@@ -583,6 +606,13 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
         __syncwarp();
         fetch_row(S0, c, ys - 1);
         fetch_row(S1, c, ys);
+        prepare<DISP, GEN, T, VM>(S0, c);
+        prepare<DISP, GEN, T, VM>(S1, c);
+    } else if (TMA_ON<T, MODE, GEN, VM>) {
+        // prologue: rows ys-1 (S0), ys (S1) from the ring, prepared
+        ring::ring_row(c.tm, *c.rg, 0, c.lane, S0.raw);
+        ring::ring_row(c.tm, *c.rg, 1, c.lane, S1.raw);
+        S0.rok = S1.rok = true;
         prepare<DISP, GEN, T, VM>(S0, c);
         prepare<DISP, GEN, T, VM>(S1, c);
     } else {
@@ -625,9 +655,10 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
 // masked variants count their special row steps into p.fired (host-side AUTO, tfn_abi.cu).
 template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS, int OUT>
 #ifdef TFN_STRIP_MAXNREG
-__global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(KernelArgs p) {
+__global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(const __grid_constant__ CUtensorMap tm, KernelArgs p) {
 #else
-__global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T, KV == 1>::on ? TFN_U16_MINBLOCKS : TFN_STRIP_MINBLOCKS) tfn_strip_kernel(KernelArgs p) {
+__global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T, KV == 1>::on ? TFN_U16_MINBLOCKS : TFN_STRIP_MINBLOCKS)
+    tfn_strip_kernel(const __grid_constant__ CUtensorMap tm, KernelArgs p) {
 #endif
     const int lane = threadIdx.x & 31;
     const int warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -646,6 +677,15 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T, KV == 1>::on ? TFN_
     c.outk = (OUT == 2) ? p.out_kind : (OUT == 3 ? 2 : OUT);
     c.lane = lane;
     if constexpr (Ring<T, KV == 1>::on) c.ring = ring_base();
+    ring::Ring rg;
+    constexpr bool TMA = TMA_ON<T, MODE, KV == 1, KV == 2>;
+    if constexpr (TMA) {
+        __shared__ __align__(128) float slots[TFN_STRIP_THREADS / 32][ring::NS * ring::SLOT_FLOATS];
+        __shared__ __align__(8) unsigned long long bars[TFN_STRIP_THREADS / 32][ring::NS];
+        ring::ring_init(rg, slots[threadIdx.x >> 5], bars[threadIdx.x >> 5], lane);
+        c.rg = &rg;
+        c.tm = &tm;
+    }
     c.pscale = p.pscale; c.ifx = p.ifx; c.ify = p.ify;
     const int cb = c.outk == 0 ? 4 : 2;          // bytes per stored component
     const int nc = c.outk == 2 ? 2 : 3;          // stored components per pixel
@@ -678,7 +718,12 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T, KV == 1>::on ? TFN_
         c.pts = p.pts ? p.pts + fb * 3 * HW + (LAYOUT == 0 ? (long long)c.cm : 3LL * c.cm) : nullptr;
 
         c.y1 = y1;
+        if constexpr (TMA) {
+            ring::ring_strip(&tm, rg, sx * STRIP_COLS - 4, y0, y1, (int)fb, lane);
+            c.ys = y0;
+        }
         strip_rows<F, MODE, DISP, LAYOUT, KV == 1, T, PTS, OUT, KV == 2>(c, out, HW, colmask, y0, y1);
+        if constexpr (TMA) ring::ring_strip_done(rg);
         if (p.work) {
             int nxt = 0;
             if (lane == 0) nxt = atomicAdd(p.work, 1);

@@ -16,8 +16,8 @@ namespace tfn {
 
 template <int F, int MODE, bool DISP, int KV, class T, bool PTS = false, int OUT = 2>
 static cudaError_t launch_l(const KernelArgs& a, int grid, cudaStream_t st) {
-    if (a.layout == 0) tfn_strip_kernel<F, MODE, DISP, 0, KV, T, PTS, OUT><<<grid, TFN_STRIP_THREADS, 0, st>>>(a);
-    else tfn_strip_kernel<F, MODE, DISP, 1, KV, T, PTS, OUT><<<grid, TFN_STRIP_THREADS, 0, st>>>(a);
+    if (a.layout == 0) tfn_strip_kernel<F, MODE, DISP, 0, KV, T, PTS, OUT><<<grid, TFN_STRIP_THREADS, 0, st>>>(*a.tmap, a);
+    else tfn_strip_kernel<F, MODE, DISP, 1, KV, T, PTS, OUT><<<grid, TFN_STRIP_THREADS, 0, st>>>(*a.tmap, a);
     return cudaGetLastError();
 }
 

@@ -30,3 +30,32 @@ def test_reference_arm_nonzero_rank_is_silent():
                         "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT,
                        env=env)
     assert r.returncode == 0 and not [l for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def test_gpus_flag_launches_ranks_dry_run():
+    """`--gpus 2` outside torchrun re-launches bench.py under torch.distributed.run with two
+    ranks (gloo in the dry run): one JSON line, n_gpus == 2, disjoint frame shards."""
+    for cfg, strong in ((2, False), (5, True)):
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--dry-run", "--gpus", "2",
+                            "--config", str(cfg), "--steps", "3", "--warmup", "1"],
+                           capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert r.returncode == 0, r.stderr[-3000:]
+        lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+        assert len(lines) == 1, r.stdout
+        d = json.loads(lines[0])
+        assert d["n_gpus"] == 2 and d["dry_run"] and d["steps"] == 3
+        (a0, b0), (a1, b1) = d["config"]["rank_frames"]
+        assert b0 <= a1 and a0 < b0 and a1 < b1            # disjoint, ordered
+        if strong:
+            assert (a0, b1) == (0, 65536) and b0 == a1     # the fixed total, covered once
+            assert d["scaling"] == "strong"
+        else:
+            assert b0 - a0 == b1 - a1 == 1024 and d["scaling"] == "weak"
+
+
+def test_gpus_flag_single_rank_dry_run():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--dry-run", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["n_gpus"] == 1 and d["config"]["rank_frames"] == [[0, 1024]]

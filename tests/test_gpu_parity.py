@@ -413,7 +413,7 @@ def test_masked_kernel_bitwise_vs_pixel(tfn, cfg1, random8):
     from paper_2005_08165_b200 import tfn as T
     est = tfn.Estimator(ts.K_VGA, "sobel", "median")
     with pytest.raises(T.TfnError):
-        T.tfn_set_option(est.h, T.OPT_KERNEL, 5)          # 0 auto .. 4 masked
+        T.tfn_set_option(est.h, T.OPT_KERNEL, 7)          # 0 auto .. 6 fp32 masked
     for name, z, K, disp in _general_cases(cfg1, random8):
         for f in FILTERS:
             for m in MODES:
@@ -609,3 +609,35 @@ def test_extreme_disparity_and_noise(tfn, random8, scale):
         for f in FILTERS:
             for m in MODES:
                 check(tfn, z, ts.K_VGA, f, m)
+
+
+def test_graph_counter_never_shared_with_direct_calls(tfn, random8):
+    """a launch captured into a CUDA graph keeps its own work counter.  Capture a
+    dynamically scheduled launch, make > 4096 direct calls (the direct-call ring wraps), then
+    replay the graph on one stream while direct calls run on another: the replayed output is
+    bit-identical to the uncaptured result every time."""
+    x = random8.depth.cuda().repeat(8, 1, 1)                   # 64 frames: more strips than warps
+    est = tfn.Estimator(ts.K_VGA, "sobel", "median", kernel="strip")
+    ref = est.estimate(x).clone()
+    out = torch.empty_like(ref)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    s1.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s1):
+        with torch.cuda.graph(g, stream=s1):
+            est.estimate(x, out=out, stream=s1)
+    torch.cuda.synchronize()
+    small = x[:16]
+    scratch = torch.empty((16, 3, 480, 640), device="cuda")
+    for _ in range(4100):                                     # the direct ring (4096 pairs) wraps
+        est.estimate(small, out=scratch, stream=s2)
+    torch.cuda.synchronize()
+    for _ in range(6):
+        out.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(s1):
+            g.replay()
+        for _ in range(4):
+            est.estimate(small, out=scratch, stream=s2)      # concurrent direct calls
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int32), ref.view(torch.int32))

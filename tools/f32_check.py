@@ -64,9 +64,14 @@ if __name__ == "__main__":
     if "time" in what:
         sc = ts.random_scenes(1024, K, 480, 640, seed=0)
         x = ts.render(sc, K, 480, 640, device="cuda").depth
-        for k in ("strip", "f32", "f32masked"):
+        ks = ("strip", "f32", "f32masked")
+        for w in what:
+            if w.startswith("kernels="):
+                ks = tuple(w.split("=")[1].split(","))
+        for k in ks:
             timeit(K, "sobel", "median", k, x)
-        timeit(K, "sobel", "mean", "f32", x)
+        for k in ks:
+            timeit(K, "sobel", "mean", k, x)
         del x
     if "parity" in what:
         c1 = ts.render(ts.config1_scene(), K, 480, 640).depth.numpy()
