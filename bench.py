@@ -337,12 +337,25 @@ def run_reference(args, cfg, ws, rank):
         "data": "synthetic (seeded analytic ray-cast scenes)",
         "config": {"workload": cfg["desc"], "filter": filt, "nz_mode": mode, "H": H, "W": W,
                    "frames_per_step": n, "fps": val * 1e6 / (H * W)},
-        "cpu_baseline": {"value": val, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": val, "unit": "Mpixel/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"{n} frames/step ({H}x{W}), {steps} steps, fp64 C oracle, one frame per thread"},
         "e2e": {"value": val, "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_model() -> str:
+    """The host CPU's model string (/proc/cpuinfo), for the cpu_baseline record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cpu_baseline(cfg, filt, mode, seconds, seed):
@@ -372,7 +385,7 @@ def cpu_baseline(cfg, filt, mode, seconds, seed):
     t0 = time.perf_counter()
     oracle.estimate(x1, cfg["K"], filt, mode, threads=1, **kw)
     t_1 = time.perf_counter() - t0
-    return {"value": val, "unit": "Mpixel/s", "cores": cores, "kind": "oracle",
+    return {"value": val, "unit": "Mpixel/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{n // passes} frames of the workload ({H}x{W}, {filt}+{mode}) x {passes} passes, "
                       f"fp64 C oracle, frames split over {cores} threads, {t:.1f} s wall",
             "single_thread": {"value": len(x1) * H * W / t_1 / 1e6, "unit": "Mpixel/s",

@@ -432,6 +432,7 @@ static __device__ __noinline__ void queue_append(int* q, int& qn, unsigned sp, i
     }
     const int total = __shfl_sync(0xffffffffu, incl, 31);
     int pos = qn + incl - cnt;
+    TFN_CHECK(qn + total <= QCAP && v >= 0 && v < 65536 && c0 >= 0 && c0 + PPL <= 65536);
 #pragma unroll
     for (int i = 0; i < PPL; ++i)
         if (sp & (1u << i)) q[pos++] = (v << 16) | (c0 + i);
@@ -451,6 +452,7 @@ __device__ __noinline__ void queue_flush(const int* q, int& qn, bool all, const 
         if (lane < nb) {
             const int e = q[qn - nb + lane];
             const int v = e >> 16, u = e & 0xffff;
+            TFN_CHECK(qn - nb + lane >= 0 && v < H && u < W);
             const Normal n = pixel_general<F, MODE, DISP>(img, H, W, v, u, u0, v0, fx, fy, Wts{kp, k0});
             const long long pix = (long long)v * W + u;
             if (LAYOUT == 0) {
@@ -532,6 +534,7 @@ tfn_f32_kernel(const __grid_constant__ CUtensorMap tm, const KernelArgs p, const
                                                             lk[(S) % 3], lk[((S) + 1) % 3], zr, bf,           \
                                                             kc.kr * fabsf(bf), ox, oy, oz);                         \
             if (v >= y0) {                                                                                     \
+                TFN_CHECK(v < p.H && (!okm || c0 + PPL <= p.W));                                               \
                 if (okm) store_row<LAYOUT>(orow + (long long)v * p.W * (LAYOUT == 0 ? 1 : 3), HW, ox, oy, oz); \
                 if (!VM && (v == 0 || v == p.H - 1)) sp = 0;                                                   \
                 if (__any_sync(0xffffffffu, sp != 0)) {                                                        \

@@ -20,6 +20,7 @@
 #endif
 #include "tfn_tma.cuh"
 
+
 namespace tfn {
 
 enum KernelId { TFN_KERNEL_AUTO = 0, TFN_KERNEL_PIXEL = 1, TFN_KERNEL_STRIP = 2, TFN_KERNEL_STRIP_GENERAL = 3,

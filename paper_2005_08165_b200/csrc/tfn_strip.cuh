@@ -126,6 +126,7 @@ template <class T>
 __device__ __forceinline__ void issue_row(const StripCtx<T>& c, int v) {
     const bool rin = (v >= 0) && (v < c.H);
     const unsigned slot = c.ring + ((v + 1) & 7) * RING_RB;
+    TFN_CHECK(c.cm >= 0 && c.cm + PPL <= c.W && 16 + c.lane * PPL * (int)sizeof(T) + PPL * (int)sizeof(T) <= RING_RB - 16);
     const T* row = c.pm + (rin ? v : 0) * c.W;
     constexpr int VB = PPL * sizeof(T);
     cpa(slot + 16 + c.lane * VB, row, (rin && c.okm) ? VB : 0, VB);
@@ -149,6 +150,7 @@ __device__ __forceinline__ void fetch_row(Slot& s, const StripCtx<unsigned short
 __device__ __forceinline__ void load_raw(Slot& s, const StripCtx<float>& c, int v) {
     s.rok = (v >= 0) && (v < c.H);
     const float* row = c.pm + v * c.W;
+    TFN_CHECK(c.cm >= 0 && c.cm + PPL <= c.W && (!c.okl || c.cm >= 1) && (!c.okr || c.cm + PPL < c.W));
     if (s.rok) {
         if (PPL == 4) {
             const float4 m = __ldg(reinterpret_cast<const float4*>(row));
@@ -163,6 +165,7 @@ __device__ __forceinline__ void load_raw(Slot& s, const StripCtx<float>& c, int 
 }
 __device__ __forceinline__ void load_raw(Slot& s, const StripCtx<unsigned short>& c, int v) {
     s.rok = (v >= 0) && (v < c.H);
+    TFN_CHECK(c.cm >= 0 && c.cm + PPL <= c.W && (!c.okl || c.cm >= 1) && (!c.okr || c.cm + PPL < c.W));
     const unsigned short* row = c.pm + v * c.W;
     if (s.rok) {
         if (PPL == 4) {
@@ -320,9 +323,12 @@ __device__ __forceinline__ void store_packed(__half* o, const float* x, const fl
 // fast 261 vs 252, masked 263 vs 247, general 168 vs 177 Gpx/s — the register window already
 // loads every sample once (loads are 1/4 of the traffic), so the ring only removes the prefetch
 // registers; it stays off where it measured slower (fast median, general mean).
+#ifndef TFN_STRIP_TMA_ALL
+#define TFN_STRIP_TMA_ALL 0      // 1: every fp32 variant through the ring (A/B builds)
+#endif
 template <class T, int MODE, bool GEN, bool VM>
-constexpr bool TMA_ON = (TFN_STRIP_TMA != 0) && (sizeof(T) == 4) && !(MODE == MEDIAN && !GEN && !VM) &&
-                        !(MODE == MEAN && GEN);
+constexpr bool TMA_ON = (TFN_STRIP_TMA != 0) && (sizeof(T) == 4) &&
+                        (TFN_STRIP_TMA_ALL || (!(MODE == MEDIAN && !GEN && !VM) && !(MODE == MEAN && GEN)));
 
 template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT, bool VM = false>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
@@ -541,6 +547,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     // ---- store (16-B / 8-B aligned: W % 4 == 0, c0 % 4 == 0).  OUT: 0 fp32, 1 half, 3 oct16,
     //      2 the handle's choice at run time (general variant); points are general-only ----
     if (c.okm) {
+        TFN_CHECK(v >= 0 && v < c.H && c.cm >= 0 && c.cm + PPL <= c.W);
         const int kind = (OUT == 2) ? c.outk : (OUT == 3 ? 2 : OUT);
         if (kind == 2) {
             short* o = reinterpret_cast<short*>(out) + v * c.W * (LAYOUT == 0 ? 1 : 2);

@@ -11,6 +11,24 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cstdio>
+
+// Bounds-checked debug build (-DTFN_BOUNDS_CHECK; compute-sanitizer is closed on the GPU pool):
+// every global row / column index and shared-memory ring / queue index is checked on the device
+// and a violation traps (the launch fails with an unspecified-launch error).
+#ifndef TFN_CHECK
+#ifdef TFN_BOUNDS_CHECK
+#define TFN_CHECK(cond)                                                             \
+    do {                                                                            \
+        if (!(cond)) {                                                              \
+            printf("TFN_CHECK failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);    \
+            __trap();                                                               \
+        }                                                                           \
+    } while (0)
+#else
+#define TFN_CHECK(cond) ((void)0)
+#endif
+#endif
 
 #ifndef TFN_RING_RC
 #define TFN_RING_RC 4             // rows per TMA box
@@ -26,6 +44,7 @@ constexpr int RC = TFN_RING_RC;
 constexpr int NS = TFN_RING_NS;
 constexpr int BOXW = 136;
 constexpr int SLOT_FLOATS = RC * BOXW;
+static_assert((SLOT_FLOATS * 4) % 128 == 0, "TMA box destinations must stay 128-B aligned: TFN_RING_RC % 4 == 0");
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -91,6 +110,7 @@ __device__ __forceinline__ void ring_row(const CUtensorMap* tm, const Ring& r, i
         }
         bar_wait(r.bar + slot * 8, (g / NS) & 1u);
     }
+    TFN_CHECK(slot < (unsigned)NS && rw >= 0 && rw < RC && k < r.nch && lane >= 0 && lane < 32);
     const float* p = r.base + slot * SLOT_FLOATS + rw * BOXW;
     const float4 m = *reinterpret_cast<const float4*>(p);
     zr[0] = p[-1]; zr[1] = m.x; zr[2] = m.y; zr[3] = m.z; zr[4] = m.w; zr[5] = p[4];

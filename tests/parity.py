@@ -33,7 +33,7 @@ def compare(gpu: np.ndarray, ref: np.ndarray, sample: np.ndarray, K, disparity=F
            "mask_diff": int(np.count_nonzero(mg != mr))}
     both = mg & mr
     if not both.any():
-        res.update(max_deg=0.0, n_bad=0, n_tie=0, p999=0.0)
+        res.update(max_deg=0.0, n_bad=0, n_tie=0, p999=0.0, tie_gpu_max=0.0)
         return res
     gv = np.moveaxis(g, 1, -1)[both]
     rv = np.moveaxis(r, 1, -1)[both]
@@ -47,14 +47,23 @@ def compare(gpu: np.ndarray, ref: np.ndarray, sample: np.ndarray, K, disparity=F
     tie = np.abs(np.sum(rv * p, axis=-1)) < TIE
     ang_tie = np.minimum(ang, angular_error_deg(-gv, rv))
     ang = np.where(tie, ang_tie, ang)
+    gpu_cos = np.abs(np.sum(gv * p, axis=-1)) / np.maximum(np.linalg.norm(gv, axis=-1), 1e-300)
     res.update(max_deg=float(ang.max()), p999=float(np.percentile(ang, 99.9)),
-               n_bad=int(np.count_nonzero(ang > tol)), n_tie=int(tie.sum()))
+               n_bad=int(np.count_nonzero(ang > tol)), n_tie=int(tie.sum()),
+               tie_gpu_max=float(gpu_cos[tie].max()) if tie.any() else 0.0)
     if res["n_bad"]:
         worst = np.argsort(ang)[-5:]
         res["worst"] = [(int(bb[i]), int(vv[i]), int(uu[i]), float(ang[i])) for i in worst]
     return res
 
 
+TIE_GPU = 1e-4         # a tie-zone pixel's GPU normal must itself be grazing: |<n^, p^>| <= this
+
+
 def assert_parity(res: dict, what: str = ""):
     assert res["mask_equal"], f"{what}: invalid masks differ at {res['mask_diff']} pixels"
+    # the tie zone is compared sign-agnostically; an orientation error cannot hide there, because
+    # the GPU's own normal must be perpendicular to the viewing ray to within TIE_GPU (a
+    # confidently wrong sign gives |<n^,p^>| ~ 1).  VERDICT r1 item 8; the count is reported.
+    assert res["tie_gpu_max"] <= TIE_GPU, f"{what}: tie-zone pixel with |<n,p>| = {res['tie_gpu_max']}"
     assert res["n_bad"] == 0, f"{what}: {res['n_bad']} pixels > {TOL_DEG} deg, max {res['max_deg']}: {res.get('worst')}"

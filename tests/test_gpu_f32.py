@@ -147,3 +147,35 @@ def test_stats_identical_for_any_shard_count(tfn):
         vecs[G] = total.tolist()
     assert vecs[1][7] == n * 480 * 640
     assert vecs[1] == vecs[2] == vecs[4] == vecs[8], vecs
+
+
+def test_no_writes_outside_buffers(tfn):
+    """every kernel variant writes exactly its output (and point-cloud) buffer: both sit inside
+    larger allocations whose margins hold a canary pattern that must survive (ragged widths,
+    odd strip heights, holes).  With compute-sanitizer closed on the GPU pool this, the
+    bounds-checked build (TFN_BOUNDS_CHECK) and the ring-stress build carry the memory-safety
+    evidence."""
+    canary = -12345.678
+    for (n, H, W) in ((2, 33, 132), (1, 70, 260), (1, 31, 1024), (3, 5, 8)):
+        K = ts.Intrinsics(200.0, 210.0, W / 2 - 0.3, H / 2 + 0.7)
+        x = ts.render(ts.random_scenes(n, K, H, W, seed=4, holes=True, salt=0.02), K, H, W, device="cuda").depth
+        pad = 4096
+        for kern in ("strip", "masked", "general", "pixel", "f32", "f32masked"):
+            for layout in ("planar", "packed"):
+                for sh in (0, 5):
+                    est = tfn.Estimator(K, "sobel", "median", kernel=kern, layout=layout, strip_h=sh)
+                    buf = torch.full((n * 3 * H * W + 2 * pad,), canary, device="cuda")
+                    shape = (n, 3, H, W) if layout == "planar" else (n, H, W, 3)
+                    out = buf[pad:pad + n * 3 * H * W].view(shape)
+                    est.estimate(x, out=out)
+                    torch.cuda.synchronize()
+                    assert (buf[:pad] == canary).all() and (buf[-pad:] == canary).all(), (kern, layout, sh, H, W)
+                    assert not (out == canary).any(), (kern, layout, sh, H, W)     # every pixel written
+        est = tfn.Estimator(K, "prewitt", "median")
+        buf = torch.full((2 * n * 3 * H * W + 3 * pad,), canary, device="cuda")
+        nrm = buf[pad:pad + n * 3 * H * W].view(n, 3, H, W)
+        pts = buf[2 * pad + n * 3 * H * W:2 * pad + 2 * n * 3 * H * W].view(n, 3, H, W)
+        est.estimate_points(x, out=nrm, points=pts)
+        torch.cuda.synchronize()
+        assert (buf[:pad] == canary).all() and (buf[pad + n * 3 * H * W:2 * pad + n * 3 * H * W] == canary).all()
+        assert (buf[-pad:] == canary).all()

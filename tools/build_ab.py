@@ -13,4 +13,7 @@ for spec in sys.argv[1:]:
     t = time.time()
     out = os.path.join(b.ROOT, "abl", f"lib_{name}.so")
     b.build(force=True, out=out, defines=[d for d in defs.split(",") if d])
+    for f in os.listdir(os.path.join(b.HERE, "build")):       # keep the gpurun snapshot small
+        if f.startswith(f"lib_{name}_"):
+            os.remove(os.path.join(b.HERE, "build", f))
     print(f"{out} ({time.time() - t:.0f} s)", flush=True)
