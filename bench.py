@@ -528,7 +528,8 @@ def main():
     variant = {"auto": {2: "fast strip (AUTO)", 3: "general strip (AUTO)", 4: "masked strip (AUTO)"}.get(
                    _T.tfn_auto_variant(est.h)),
                "strip": "fast strip", "general": "general strip", "masked": "masked strip",
-               "pixel": "per-pixel"}[args.kernel]
+               "pixel": "per-pixel", "f32": "fp32 unit-step (tfn_f32_kernel)",
+               "f32masked": "fp32 unit-step masked (tfn_f32_kernel)"}[args.kernel]
     if cfg.get("u16") and args.kernel in ("auto", "strip"):
         variant = "general strip (uint16 input)"
 
@@ -637,7 +638,8 @@ def main():
                          "algorithmic_GB_per_launch": bytes_px * px_per_launch / 1e9,
                          "sol_same_mix_GBps": sol, "frac_of_sol": (achieved / sol) if sol else None,
                          "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                         "kernel": "tfn_strip_kernel", "bytes_per_px": bytes_px,
+                         "kernel": "tfn_f32_kernel" if args.kernel.startswith("f32") else "tfn_strip_kernel",
+                         "bytes_per_px": bytes_px,
                          "px_per_launch": px_per_launch, "launch_ms": per_launch_ms},
             "e2e": e2e, "gpu_launches": int(launches) if not use_graph else steps, "clocks": clk.summary(),
             "cuda_graph": bool(use_graph),

@@ -19,9 +19,11 @@ for v in rows[2:]:
         except (KeyError, ValueError):
             return default
     print(d.get("Kernel Name", "")[:100])
-    dur = g("gpu__time_duration.sum")
-    print(f"duration {dur / 1e3:.1f} us  dram rd {g('dram__bytes_read.sum') / 1e6:.1f} MB wr {g('dram__bytes_write.sum') / 1e6:.1f} MB"
-          f"  dram {g('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.1f}%")
+    un = dict(zip(h, units))
+    print(f"duration {d.get('gpu__time_duration.sum')} {un.get('gpu__time_duration.sum')}  "
+          f"dram read {d.get('dram__bytes_read.sum')} {un.get('dram__bytes_read.sum')}  "
+          f"write {d.get('dram__bytes_write.sum')} {un.get('dram__bytes_write.sum')}  "
+          f"dram {g('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed'):.1f}% of peak")
     inst = g("smsp__inst_executed.sum")
     print(f"warp-inst {inst:.4g}" + (f"  thread-inst/px {inst * 32 / px:.1f}" if px else "") +
           f"  issue-active {g('sm__inst_issued.avg.pct_of_peak_sustained_active'):.1f}%"
