@@ -41,6 +41,9 @@
 #ifndef TFN_STRIP_PPL
 #define TFN_STRIP_PPL 4          // pixels (columns) per lane: 4 or 2
 #endif
+#ifndef TFN_PHI_EXT
+#define TFN_PHI_EXT 1            // median fast / masked: finiteness from the network's extremes, no candidate sum
+#endif
 #ifndef TFN_STRIP_TMA
 #define TFN_STRIP_TMA 1          // fp32 input rows through the per-warp TMA ring (tfn_tma.cuh) instead of
 #endif                           // the three-rows-ahead register prefetch
@@ -435,6 +438,16 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
                                   : __ffma2_rn(x, f2(R[0][k], R[1][k]), (k & 1) ? f2(-m.x, -m.y) : m);
                 }
             }
+        } else if (TFN_PHI_EXT && !GEN) {
+            // median, fast / masked: candidates only — finiteness comes from the network (mid_pair8_ext)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float2 x = (k < 2) ? xu : (k < 4) ? xv : (k < 6) ? xs : xt;
+                const float2 m = (k < 2) ? mu : (k < 4) ? mv : (k < 6) ? ms : mt;
+                tau[k] = DISP ? __fmul2_rn(x, f2(R[0][k], R[1][k]))
+                              : __ffma2_rn(x, f2(R[0][k], R[1][k]), (k & 1) ? f2(-m.x, -m.y) : m);
+            }
+            sum8 = f2(0.f, 0.f);
         } else if (DISP) {
 #pragma unroll
             for (int k = 0; k < 8; k += 2) {
@@ -492,8 +505,15 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
 #pragma unroll
             for (int k = 0; k < 8; ++k) { t0[k] = tau[k].x; t1[k] = tau[k].y; }
             float a0, b0, a1, b1;
-            mid_pair8(t0, a0, b0);
-            mid_pair8(t1, a1, b1);
+            if (TFN_PHI_EXT) {
+                float e0, e1;
+                mid_pair8_ext(t0, a0, b0, e0);
+                mid_pair8_ext(t1, a1, b1, e1);
+                sum8 = f2(e0, e1);       // finite iff all 8 candidates are
+            } else {
+                mid_pair8(t0, a0, b0);
+                mid_pair8(t1, a1, b1);
+            }
             phi = __fmul2_rn(__fadd2_rn(f2(a0, a1), f2(b0, b1)), f2(0.5f, 0.5f));
             // FMNMX drops NaN candidates: make Phi NaN when any candidate is non-finite, so
             // pixels with out-of-image taps (the border, never "special") come out NaN
