@@ -7,7 +7,9 @@ A step is one pass of the whole hot path (one fused
 kernel launch) over one batch of synthetic frames resident in HBM.  Default
 workload = BASELINE.json configs[1]: 1024 x 480x640 depth frames, Sobel + median,
 planar fp32 normals, per GPU (weak scaling: each rank renders its own frames).
-Inputs (1.26 GB) exceed the 126 MB L2, so no flush is needed between steps.
+Inputs (1.26 GB) exceed the 126 MB L2, so no flush is needed between steps; workloads whose
+inputs fit in L2 (configs[0], one frame) get a 512 MB L2 flush between steps, outside the
+per-step CUDA events that time them.
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the fp64 CPU oracle
 (oracle/, the only non-test code allowed to run it) on the same config/metric.
@@ -475,6 +477,10 @@ def main():
         step = g.replay
 
     steps = args.steps
+    # timing rule: inputs smaller than the 126 MB L2 (configs[0], small --frames / --hw) get an L2
+    # flush (a 512 MB write) between timed steps, and the steps are timed by their own events
+    in_bytes = chunk * H * W * in_b
+    l2_flush = torch.empty(128 << 20, dtype=torch.float32, device=dev) if in_bytes < (256 << 20) and not streaming_cfg else None
     chunk_list = list(tdist.chunks(first, last, chunk))
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     launches0 = tfn.tfn_kernel_launches()
@@ -513,6 +519,8 @@ def main():
         with clk:
             t_all0.record(stream)
             for s in range(steps):
+                if l2_flush is not None:
+                    l2_flush.fill_(s)           # evict the step's input / output from L2 (outside the events)
                 ev[s][0].record(stream)
                 step()
                 ev[s][1].record(stream)
@@ -522,6 +530,8 @@ def main():
             pg.barrier()
         total_ms = t_all0.elapsed_time(t_all1)
         kernel_ms = sum(a.elapsed_time(b) for a, b in ev)
+        if l2_flush is not None:
+            total_ms = kernel_ms                # flushes are between the timed steps, not in them
         units = per_rank * H * W * steps
     launches = tfn.tfn_kernel_launches() - launches0
     from paper_2005_08165_b200 import tfn as _T
@@ -631,7 +641,8 @@ def main():
                        "input": "disparity" if cfg["disp"] else ("depth u16 mm codes" if cfg.get("u16") else "depth"),
                        "out_dtype": out_dtype, "kernel_variant": variant, "frames_per_gpu": per_rank,
                        "H": H, "W": W, "fps": value * 1e6 / (H * W),
-                       "l2": "inputs (%.2f GB/GPU) larger than the 126 MB L2; no flush" % (chunk * H * W * in_b / 1e9),
+                       "l2": ("inputs (%.2f GB/GPU) larger than the 126 MB L2; no flush" % (in_bytes / 1e9)) if l2_flush is None
+                             else "inputs (%.4f GB/GPU) fit in L2: 512 MB L2 flush between steps, outside the per-step CUDA events" % (in_bytes / 1e9),
                        "parallelism": f"dp{ws} (frame batches sharded, no collective on the hot path)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_unit": "GB/launch (ncu dram read+write)",
