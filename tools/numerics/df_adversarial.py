@@ -1,4 +1,4 @@
-"""Adversarial check of the double-float (fp32 hi + lo) gradient idea (tools/ws/df_emul.py): random 3x3
+"""Adversarial check of the double-float (fp32 hi + lo) gradient idea (tools/numerics/df_emul.py): random 3x3
 windows split by a line into two planes with a 1.1-3x depth ratio; angle of the normal from
 double-float gradients vs exact fp64 gradients at the window centre.  DESIGN §12."""
 import numpy as np, sys
