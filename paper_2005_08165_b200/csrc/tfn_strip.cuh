@@ -671,6 +671,19 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
     }
 }
 
+// resident CTAs per SM the register budget is sized for: 3 (168 registers, 12 warps) by
+// default; the uint16 ring instantiations 4 (128); the fp32 FD + mean fast / masked
+// instantiations TFN_STRIP_MINBLOCKS_FDMEAN (no median network, no corner taps: the only ones
+// that fit 128 registers without spills)
+#ifndef TFN_STRIP_MINBLOCKS_FDMEAN
+#define TFN_STRIP_MINBLOCKS_FDMEAN 4        // measured: FD + mean 274.5 -> 290.7 Gpx/s (16 vs 12 warps/SM; XU-bound, r02)
+#endif
+template <int F, int MODE, int KV, class T>
+constexpr int strip_minblocks() {
+    return Ring<T, KV == 1>::on ? TFN_U16_MINBLOCKS
+           : (F == FD && MODE == MEAN && KV != 1) ? TFN_STRIP_MINBLOCKS_FDMEAN : TFN_STRIP_MINBLOCKS;
+}
+
 // KV (kernel variant): 0 fast path + exact per-pixel special path, 1 general (no special
 // path: skips, flat, ties and invalid taps resolved in registers; ~45 % more instructions
 // per pixel, but no divergent exact-path calls — the better choice when many row steps
@@ -684,7 +697,7 @@ template <int F, int MODE, bool DISP, int LAYOUT, int KV, class T, bool PTS, int
 #ifdef TFN_STRIP_MAXNREG
 __global__ void __maxnreg__(TFN_STRIP_MAXNREG) tfn_strip_kernel(const __grid_constant__ CUtensorMap tm, KernelArgs p) {
 #else
-__global__ void __launch_bounds__(TFN_STRIP_THREADS, Ring<T, KV == 1>::on ? TFN_U16_MINBLOCKS : TFN_STRIP_MINBLOCKS)
+__global__ void __launch_bounds__(TFN_STRIP_THREADS, strip_minblocks<F, MODE, KV, T>())
     tfn_strip_kernel(const __grid_constant__ CUtensorMap tm, KernelArgs p) {
 #endif
     const int lane = threadIdx.x & 31;
