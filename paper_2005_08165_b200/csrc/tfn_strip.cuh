@@ -44,6 +44,9 @@
 #ifndef TFN_PHI_EXT
 #define TFN_PHI_EXT 1            // median fast / masked: finiteness from the network's extremes, no candidate sum
 #endif
+#ifndef TFN_FD32
+#define TFN_FD32 1               // disparity FD + mean fast / masked: fp32 gradients (FD32_ON, fd_dw)
+#endif
 #ifndef TFN_STRIP_TMA
 #define TFN_STRIP_TMA 1          // fp32 input rows through the per-warp TMA ring (tfn_tma.cuh) instead of
 #endif                           // the three-rows-ahead register prefetch
@@ -61,6 +64,7 @@ struct Slot {
     float z[6];        // sanitized (invalid -> NaN)
     double w[6];       // x = 1/z (depth) or d (disparity), fp64
     double head[4];    // kp*D_h(row-1) + k0*D_h(row)   (D_h re-derived from w when needed)
+    float wf[6];       // FD32: x = 1/z (depth, MUFU) or d (disparity) in fp32
     float rN[4], rNW[4], rNE[4];   // pair reciprocals of the N / NW / NE neighbours (pairs owned by the row above)
     unsigned hb;       // masked variant: byte i bit 7 set iff a sample of columns i..i+2 is invalid
     unsigned cb;       //   (FD) byte i bit 7 set iff the sample of column i+1 is invalid
@@ -195,7 +199,7 @@ __device__ __forceinline__ float sanitize_fast(float z, bool ok) {
     return good ? z : __int_as_float(bad_z<VM>());
 }
 
-template <bool DISP, bool GEN, class T, bool VM = false>
+template <bool DISP, bool GEN, class T, bool VM = false, bool G32 = false>
 __device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
     // the lane's own columns need only the value test; the halos are outside the image at
     // the first / last lane of a frame row; whole rows outside the image (loads predicated
@@ -222,6 +226,11 @@ __device__ __forceinline__ void prepare(Slot& s, const StripCtx<T>& c) {
     }
     // exact for every valid sample; invalid ones give finite garbage here, but their
     // NaN z makes the pixel "special", which recomputes it exactly
+    if constexpr (G32) {
+#pragma unroll
+        for (int j = 0; j < PPL + 2; ++j) s.wf[j] = DISP ? s.z[j] : rcp_approx(s.z[j]);
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < PPL + 2; ++j) {
         // fast variant: integer widening (exact for the positive normal floats every valid
@@ -333,6 +342,31 @@ template <class T, int MODE, bool GEN, bool VM>
 constexpr bool TMA_ON = (TFN_STRIP_TMA != 0) && (sizeof(T) == 4) &&
                         (TFN_STRIP_TMA_ALL || (!(MODE == MEDIAN && !GEN && !VM) && !(MODE == MEAN && GEN)));
 
+// FD32 (fast / masked FD + mean on fp32 disparity): the gradients in fp32 (fd_dw below) — no fp64,
+// no F2F on the XU, which bounds the mean mode.  Measured (r02, configs[1]-sized batches):
+// disparity FD + mean 312 -> 336 Gpx/s; on depth each difference costs 3 fp32 ops instead of
+// one fp64 subtraction (91 vs 77 instr/px: 265 vs 291 Gpx/s) and the median is issue-bound
+// (182 vs 220), so those keep the fp64 path
+template <int F, int MODE, bool DISP, bool GEN, class T>
+constexpr bool FD32_ON = TFN_FD32 && F == FD && MODE == MEAN && DISP && !GEN && sizeof(T) == 4;
+
+// w_b - w_a for two samples: disparity x = d, so d_b - d_a; depth x = 1/z, so
+// (z_a - z_b) w_a w_b — the difference of the samples is exact (Sterbenz) or rounded once, and
+// every step is a product: a few ulp relative, whatever the cancellation in w_b - w_a
+template <bool DISP>
+__device__ __forceinline__ float fd_dw(float za, float wa, float zb, float wb) {
+    return DISP ? __fsub_rn(zb, za) : __fmul_rn(__fmul_rn(__fsub_rn(za, zb), wa), wb);
+}
+
+// the fp64 path's s, t of one FD pixel (out of line: the rare fallback of fd_dw's re-paired sums)
+template <bool DISP>
+__device__ __noinline__ float2 fd_st64(float zW, float zE, float zN, float zS) {
+    auto x64 = [](float z) { return DISP ? widen_pos(z) : rcp_rn(widen_pos(z)); };
+    const double gu = __dsub_rn(x64(zE), x64(zW));
+    const double gv = __dsub_rn(x64(zS), x64(zN));
+    return make_float2(__double2float_rn(__dadd_rn(gu, gv)), __double2float_rn(__dsub_rn(gv, gu)));
+}
+
 template <int F, int MODE, bool DISP, int LAYOUT, bool GEN, class T, bool PTS, int OUT, bool VM = false>
 __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const StripCtx<T>& c,
                                          char* __restrict__ out, long long HW,
@@ -350,7 +384,8 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
     } else {
         load_raw(C, c, v + 3);                       // prefetch three rows ahead (C.raw is free)
     }
-    prepare<DISP, GEN, T, VM>(N, c);
+    constexpr bool G32 = FD32_ON<F, MODE, DISP, GEN, T>;
+    prepare<DISP, GEN, T, VM, G32>(N, c);
     // masked variant (VM): special (below) = Phi non-finite or zero at a pixel whose Q4 taps (all 9; FD: the plus)
     // are valid.  An invalid sample is a NaN with the sign bit set, so the OR of the taps'
     // bits is negative iff one is invalid — and then the fast path has already produced the
@@ -363,6 +398,37 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         tapok = ~bad;                // bit 8i+7 set iff pixel i's taps are all valid
     }
 
+    float gu32[4], gv32[4], s32[4], t32[4];
+    if constexpr (G32) {
+        // ---- FD gradients in fp32: g_u = w_E - w_W and g_v = w_S - w_N are single
+        //      differences; s = g_u + g_v and t = g_v - g_u re-paired along the diagonals,
+        //      s = (w_E - w_N) + (w_S - w_W), t = (w_S - w_E) + (w_W - w_N).  A pair of opposite
+        //      sign can cancel: those pixels take s, t from the fp64 path (rare on surfaces) ----
+        unsigned bad = 0;
+#pragma unroll
+        for (int i = 0; i < PPL; ++i) {
+            const float zW = C.z[i], wW = C.wf[i], zE = C.z[i + 2], wE = C.wf[i + 2];
+            const float zN = P.z[i + 1], wN = P.wf[i + 1], zS = N.z[i + 1], wS = N.wf[i + 1];
+            gu32[i] = fd_dw<DISP>(zW, wW, zE, wE);
+            gv32[i] = fd_dw<DISP>(zN, wN, zS, wS);
+            const float d1 = fd_dw<DISP>(zN, wN, zE, wE), d2 = fd_dw<DISP>(zW, wW, zS, wS);
+            const float d3 = fd_dw<DISP>(zE, wE, zS, wS), d4 = fd_dw<DISP>(zN, wN, zW, wW);
+            s32[i] = __fadd_rn(d1, d2);
+            t32[i] = __fadd_rn(d3, d4);
+            const unsigned x = (__float_as_uint(d1) ^ __float_as_uint(d2)) | (__float_as_uint(d3) ^ __float_as_uint(d4));
+            bad |= (x >> 31) << i;
+        }
+        if (__any_sync(0xffffffffu, bad != 0)) {
+#pragma unroll
+            for (int i = 0; i < PPL; ++i) {
+                if (bad & (1u << i)) {
+                    const float2 st = fd_st64<DISP>(C.z[i], C.z[i + 2], P.z[i + 1], N.z[i + 1]);
+                    s32[i] = st.x;
+                    t32[i] = st.y;
+                }
+            }
+        }
+    } else {
     // ---- fp64 gradients (Eq. 15), oracle order (Q10) ----
     double gu[4], gv[4];
     double dv[6];
@@ -377,13 +443,13 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         N.head[i] = grad_head<F>(dhc, dhn, c.wt);
         gv[i] = grad_tail<F>(grad_head<F>(dv[i], dv[i + 1], c.wt), dv[i + 2], c.wt);
     }
-    float gu32[4], gv32[4], s32[4], t32[4];
 #pragma unroll
     for (int i = 0; i < PPL; ++i) {
         gu32[i] = __double2float_rn(gu[i]);
         gv32[i] = __double2float_rn(gv[i]);
         s32[i] = __double2float_rn(__dadd_rn(gu[i], gv[i]));
         t32[i] = __double2float_rn(__dsub_rn(gv[i], gu[i]));
+    }
     }
 
     // ---- rho of the 8 neighbours (order E W S N SE NW SW NE) and the next row's N/NW/NE ----
@@ -633,28 +699,29 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
         __syncwarp();
         fetch_row(S0, c, ys - 1);
         fetch_row(S1, c, ys);
-        prepare<DISP, GEN, T, VM>(S0, c);
-        prepare<DISP, GEN, T, VM>(S1, c);
+        prepare<DISP, GEN, T, VM, FD32_ON<F, MODE, DISP, GEN, T>>(S0, c);
+        prepare<DISP, GEN, T, VM, FD32_ON<F, MODE, DISP, GEN, T>>(S1, c);
     } else if (TMA_ON<T, MODE, GEN, VM>) {
         // prologue: rows ys-1 (S0), ys (S1) from the ring, prepared
         ring::ring_row(c.tm, *c.rg, 0, c.lane, S0.raw);
         ring::ring_row(c.tm, *c.rg, 1, c.lane, S1.raw);
         S0.rok = S1.rok = true;
-        prepare<DISP, GEN, T, VM>(S0, c);
-        prepare<DISP, GEN, T, VM>(S1, c);
+        prepare<DISP, GEN, T, VM, FD32_ON<F, MODE, DISP, GEN, T>>(S0, c);
+        prepare<DISP, GEN, T, VM, FD32_ON<F, MODE, DISP, GEN, T>>(S1, c);
     } else {
         // prologue: rows ys-1 (S0), ys (S1) prepared; row ys+1 (S2) loaded
         load_raw(S0, c, ys - 1);
         load_raw(S1, c, ys);
         load_raw(S2, c, ys + 1);
-        prepare<DISP, GEN, T, VM>(S0, c);
-        prepare<DISP, GEN, T, VM>(S1, c);
+        prepare<DISP, GEN, T, VM, FD32_ON<F, MODE, DISP, GEN, T>>(S0, c);
+        prepare<DISP, GEN, T, VM, FD32_ON<F, MODE, DISP, GEN, T>>(S1, c);
         load_raw(S0, c, ys + 2);
     }
 #pragma unroll
     for (int i = 0; i < PPL; ++i) {
-        S1.head[i] = grad_head<F>(Taps<F>::corners ? __dsub_rn(S0.w[i + 2], S0.w[i]) : 0.0,
-                                  __dsub_rn(S1.w[i + 2], S1.w[i]), c.wt);
+        if constexpr (!FD32_ON<F, MODE, DISP, GEN, T>)
+            S1.head[i] = grad_head<F>(Taps<F>::corners ? __dsub_rn(S0.w[i + 2], S0.w[i]) : 0.0,
+                                      __dsub_rn(S1.w[i + 2], S1.w[i]), c.wt);
         const float zc = S1.z[i + 1];
         S1.rN[i] = pair_rcp<DISP>(S0.z[i + 1], zc);
         S1.rNW[i] = pair_rcp<DISP>(S0.z[i], zc);

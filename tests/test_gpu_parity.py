@@ -13,7 +13,7 @@ import torch
 import oracle
 import tfn_scenes as ts
 from oracle import metrics
-from tests.parity import TOL_DEG, assert_parity, compare, planar
+from tests.parity import TOL_DEG, assert_kernels_agree, assert_parity, compare, fd32_variant, planar
 
 pytestmark = pytest.mark.gpu
 
@@ -409,7 +409,8 @@ def test_general_kernel_bitwise_vs_pixel(tfn, cfg1, random8):
 def test_masked_kernel_bitwise_vs_pixel(tfn, cfg1, random8):
     """kernel=4 (the fast kernel whose special path skips pixels with an invalid Q4 tap —
     their NaN is already exact — and needs no border masks: out-of-image taps are invalid
-    taps) is bit-identical to the per-pixel kernel on every hard case, both layouts."""
+    taps) is bit-identical to the per-pixel kernel on every hard case, both layouts (disparity
+    FD + mean: fp32 gradients, within FD32_TOL_DEG of it — tests/parity.py)."""
     from paper_2005_08165_b200 import tfn as T
     est = tfn.Estimator(ts.K_VGA, "sobel", "median")
     with pytest.raises(T.TfnError):
@@ -419,7 +420,7 @@ def test_masked_kernel_bitwise_vs_pixel(tfn, cfg1, random8):
             for m in MODES:
                 gp = run_gpu(tfn, z, K, f, m, disp=disp, kernel="pixel")
                 gm = run_gpu(tfn, z, K, f, m, disp=disp, kernel="masked")
-                assert np.array_equal(gm.view(np.uint32), gp.view(np.uint32)), (name, f, m)
+                assert_kernels_agree(gm, gp, fd32_variant(disp, f, m), (name, f, m))
                 gk = run_gpu(tfn, z, K, f, m, disp=disp, kernel="masked", layout="packed")
                 assert np.array_equal(gm.view(np.uint32), gk.view(np.uint32)), (name, f, m, "packed")
                 if f == "sobel" and m == "median":
@@ -592,7 +593,8 @@ def test_extreme_depth_scales_and_occlusions(tfn, random8, scale):
 @pytest.mark.parametrize("scale", [1e-3, 1.0, 1e3])
 def test_extreme_disparity_and_noise(tfn, random8, scale):
     """disparity maps scaled over six decades with 100x occlusion steps, and every filter on
-    heavily noisy depth (S:374 high preset): parity and bit-identical kernels"""
+    heavily noisy depth (S:374 high preset): parity and bit-identical kernels (disparity FD +
+    mean: within FD32_TOL_DEG, tests/parity.py)"""
     d = ts.depth_to_disparity(random8.depth64[:2], 500.0, 0.12).numpy().astype(np.float64) * scale
     rng = np.random.default_rng(int(scale * 7) + 1)
     for _ in range(40):
@@ -603,12 +605,28 @@ def test_extreme_disparity_and_noise(tfn, random8, scale):
         for m in MODES:
             g, _ = check(tfn, d, ts.K_VGA, f, m, disp=True)
             gk = run_gpu(tfn, d, ts.K_VGA, f, m, disp=True, kernel="general")
-            assert np.array_equal(g.view(np.uint32), gk.view(np.uint32)), (scale, f, m)
+            assert_kernels_agree(g, gk, fd32_variant(True, f, m), (scale, f, m))
     if scale == 1.0:
         z = ts.add_gaussian_noise(random8.depth[:2], ts.NOISE_PRESETS["high"], seed=5).numpy()
         for f in FILTERS:
             for m in MODES:
                 check(tfn, z, ts.K_VGA, f, m)
+
+
+def test_fd32_disparity_cancellation_fallback(tfn):
+    """disparity FD + mean runs fp32 gradients with s and t re-paired along the diagonals; a
+    saddle d = 1 + 1e-2 (u - v) + kappa (u + v)^2 puts s = g_u + g_v through zero along u + v = c,
+    where the two diagonal differences have opposite signs and the pixel takes the fp64 s, t
+    (fd_st64): parity with the oracle on both sides of the line, every variant, three curvatures"""
+    H, W = 96, 160
+    v, u = np.mgrid[0:H, 0:W].astype(np.float64)
+    for kappa in (1e-6, 1e-5, 1e-4):
+        d = 2.0 + 1e-2 * (u - v) + kappa * (u + v - 120.0) ** 2
+        d = d.astype(np.float32)[None]
+        g, _ = check(tfn, d, ts.K_VGA, "fd", "mean", disp=True)
+        for k in ("masked", "general", "pixel"):
+            gk = run_gpu(tfn, d, ts.K_VGA, "fd", "mean", disp=True, kernel=k)
+            assert_kernels_agree(g, gk, k in ("general", "pixel"), (kappa, k))
 
 
 def test_graph_counter_never_shared_with_direct_calls(tfn, random8):
