@@ -4,19 +4,22 @@
 // Geometry.  One warp owns a strip of 32*PPL columns (PPL = 4: 128) x strip_h rows of one
 // frame; each lane owns PPL adjacent columns and walks down the strip with a rolling
 // window of three row "slots" (rows v-1, v, v+1).  The row loop is unrolled by 3 and the
-// slots rotate by renaming (no register copies).  Per lane-row: fp32 input one LDG.128 +
-// two predicated halo loads, prefetched three rows ahead into registers; uint16 input one
-// cp.async of 8 B into a per-warp shared-memory ring TFN_CPA_D rows ahead (halo words by
-// the edge lanes), read back with LDS; out: three STG.128 (fp32) / STG.64 (half) / one or
-// two vector stores (oct16).  Persistent grid; strips handed out by an atomic work counter
-// (dynamic scheduling).
+// slots rotate by renaming (no register copies).  Per lane-row, fp32 input: rows of 136
+// columns x 4 arrive as TMA boxes in a per-warp shared-memory ring (tfn_tma.cuh; the fast
+// median variant instead loads one LDG.128 + two predicated halo loads three rows ahead into
+// registers — measured faster there); uint16 input: one cp.async of 8 B into a per-warp ring
+// TFN_CPA_D rows ahead (halo words by the edge lanes), read back with LDS; out: three STG.128
+// (fp32) / STG.64 (half) / one or two vector stores (oct16).  Persistent grid (12 warps/SM;
+// FD + mean 16); strips handed out by an atomic work counter (dynamic scheduling).
 //
-// Arithmetic (bit-identical to tfn_pixel_kernel, see tfn_device.cuh):
+// Arithmetic (bit-identical to tfn_pixel_kernel, see tfn_device.cuh, except FD32 below):
 //   fp64:  w = 1/z (faithful, ~2^-66), D_h, D_v, g_u, g_v in the oracle's order,
 //          s = g_u + g_v, t = g_v - g_u, rounded once to fp32;
 //   fp32:  one MUFU reciprocal per neighbour PAIR (shared by both pixels of the pair),
-//          tau = fma(m Z_c, R, +-m), Phi (24-op median network / mean), n_z, normalise,
+//          tau = fma(m Z_c, R, +-m), Phi (24-op median network with NaN-propagating
+//          min / max and an extreme-magnitude finiteness test / mean), n_z, normalise,
 //          orient — packed FMUL2/FFMA2/FADD2 over pixel pairs (0,1), (2,3).
+//   FD32:  disparity FD + mean fast / masked only — the gradients in fp32.
 // Three variants (KV), bit-identical, picked at run time by AUTO (tfn_abi.cu):
 //   fast (0):    all 8 candidates finite and Phi != 0 (no skips, no flat rule, no
 //                orientation tie, valid pixel) in registers; anything else ("special":
