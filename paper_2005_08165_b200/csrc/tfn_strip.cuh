@@ -341,9 +341,13 @@ __device__ __forceinline__ void store_packed(__half* o, const float* x, const fl
 #ifndef TFN_STRIP_TMA_ALL
 #define TFN_STRIP_TMA_ALL 0      // 1: every fp32 variant through the ring (A/B builds)
 #endif
-template <class T, int MODE, bool GEN, bool VM>
+#ifndef TFN_FD_MEDIAN16
+#define TFN_FD_MEDIAN16 1        // FD + median fast / masked: TMA ring + 16 warps/SM (128 registers, no spills): 220 -> 231 Gpx/s
+#endif
+template <int F, class T, int MODE, bool GEN, bool VM>
 constexpr bool TMA_ON = (TFN_STRIP_TMA != 0) && (sizeof(T) == 4) &&
-                        (TFN_STRIP_TMA_ALL || (!(MODE == MEDIAN && !GEN && !VM) && !(MODE == MEAN && GEN)));
+                        (TFN_STRIP_TMA_ALL || (TFN_FD_MEDIAN16 && F == FD && !GEN) ||
+                         (!(MODE == MEDIAN && !GEN && !VM) && !(MODE == MEAN && GEN)));
 
 // FD32 (fast / masked FD + mean on fp32 disparity): the gradients in fp32 (fd_dw below) — no fp64,
 // no F2F on the XU, which bounds the mean mode.  Measured (r02, configs[1]-sized batches):
@@ -381,7 +385,7 @@ __device__ __forceinline__ void row_step(Slot& P, Slot& C, Slot& N, int v, const
         cpa_wait<TFN_CPA_D - 2>();
         __syncwarp();                                // halo words come from the neighbour lanes' copies
         fetch_row(N, c, v + 1);
-    } else if (TMA_ON<T, MODE, GEN, VM>) {
+    } else if (TMA_ON<F, T, MODE, GEN, VM>) {
         ring::ring_row(c.tm, *c.rg, v + 2 - c.ys, c.lane, N.raw);   // row v+1 from the TMA ring
         N.rok = true;                                // rows outside the image arrive zero-filled
     } else {
@@ -704,7 +708,7 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
         fetch_row(S1, c, ys);
         prepare<DISP, GEN, T, VM, FD32_ON<F, MODE, DISP, GEN, T>>(S0, c);
         prepare<DISP, GEN, T, VM, FD32_ON<F, MODE, DISP, GEN, T>>(S1, c);
-    } else if (TMA_ON<T, MODE, GEN, VM>) {
+    } else if (TMA_ON<F, T, MODE, GEN, VM>) {
         // prologue: rows ys-1 (S0), ys (S1) from the ring, prepared
         ring::ring_row(c.tm, *c.rg, 0, c.lane, S0.raw);
         ring::ring_row(c.tm, *c.rg, 1, c.lane, S1.raw);
@@ -751,7 +755,8 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
 template <int F, int MODE, int KV, class T>
 constexpr int strip_minblocks() {
     return Ring<T, KV == 1>::on ? TFN_U16_MINBLOCKS
-           : (F == FD && MODE == MEAN && KV != 1) ? TFN_STRIP_MINBLOCKS_FDMEAN : TFN_STRIP_MINBLOCKS;
+           : (F == FD && MODE == MEAN && KV != 1) ? TFN_STRIP_MINBLOCKS_FDMEAN
+           : (TFN_FD_MEDIAN16 && F == FD && KV != 1) ? 4 : TFN_STRIP_MINBLOCKS;
 }
 
 // KV (kernel variant): 0 fast path + exact per-pixel special path, 1 general (no special
@@ -788,7 +793,7 @@ __global__ void __launch_bounds__(TFN_STRIP_THREADS, strip_minblocks<F, MODE, KV
     c.lane = lane;
     if constexpr (Ring<T, KV == 1>::on) c.ring = ring_base();
     ring::Ring rg;
-    constexpr bool TMA = TMA_ON<T, MODE, KV == 1, KV == 2>;
+    constexpr bool TMA = TMA_ON<F, T, MODE, KV == 1, KV == 2>;
     if constexpr (TMA) {
         __shared__ __align__(128) float slots[TFN_STRIP_THREADS / 32][ring::NS * ring::SLOT_FLOATS];
         __shared__ __align__(8) unsigned long long bars[TFN_STRIP_THREADS / 32][ring::NS];
