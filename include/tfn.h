@@ -184,7 +184,10 @@ int tfn_stats(const float* est, const float* gt, int batch, int H, int W, int la
 
 /* Probe of the device Phi (P8): for n groups of 8 candidates (device fp32 [n,8];
  * a non-finite candidate is skipped) writes Phi (mean or median of the finite ones)
- * to out_dev[n] and their count to k_dev[n], through the kernel's own code path. */
+ * to out_dev[n] and their count to k_dev[n], through the kernel's own code path.
+ * nz_mode: TFN_NZ_MEAN, TFN_NZ_MEDIAN (the per-pixel / general path), or 2 = the median as
+ * the strip kernel's fast and masked variants decide it (NaN-propagating network and its
+ * extreme-magnitude finiteness test; same results).  INVALID_ARGUMENT otherwise. */
 int tfn_debug_phi8(const float* cand_dev, long long n, int nz_mode, float* out_dev, int* k_dev,
                    void* stream);
 

@@ -656,7 +656,7 @@ TFN_API int tfn_stats(const float* est, const float* gt, int batch, int H, int W
 
 TFN_API int tfn_debug_phi8(const float* cand_dev, long long n, int nz_mode, float* out_dev, int* k_dev,
                            void* stream) {
-    if (n < 0 || nz_mode < 0 || nz_mode > 1) return TFN_ERR_INVALID_ARGUMENT;
+    if (n < 0 || nz_mode < 0 || nz_mode > 2) return TFN_ERR_INVALID_ARGUMENT;
     if (n == 0) return TFN_OK;
     if (!cand_dev || !out_dev || !k_dev) return TFN_ERR_INVALID_ARGUMENT;
     if (tfn::launch_phi8(cand_dev, n, nz_mode, out_dev, k_dev, (cudaStream_t)stream) != cudaSuccess)

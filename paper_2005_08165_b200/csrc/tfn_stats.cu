@@ -114,8 +114,20 @@ __global__ void tfn_phi8_kernel(const float* __restrict__ cand, long long n, flo
     const float sum8 = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
     float phi;
     int k = 8;
-    if (fabsf(sum8) < __int_as_float(0x7f800000)) phi = phi_all8<MODE>(t, sum8);
-    else phi = phi_general<MODE>(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], &k);
+    if (MODE == 2) {
+        // the strip kernel's fast / masked median (TFN_PHI_EXT): the NaN-propagating network
+        // and its extreme-magnitude test decide the fast path instead of the candidate sum
+        float u[8], v3, v4, ext;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) u[j] = t[j];
+        mid_pair8_ext(u, v3, v4, ext);
+        if (fabsf(ext) < __int_as_float(0x7f800000)) phi = __fmul_rn(__fadd_rn(v3, v4), 0.5f);
+        else phi = phi_general<MEDIAN>(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], &k);
+    } else if (fabsf(sum8) < __int_as_float(0x7f800000)) {
+        phi = phi_all8<MODE>(t, sum8);
+    } else {
+        phi = phi_general<MODE>(t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], &k);
+    }
     out[i] = phi;
     kout[i] = k;
 }
@@ -125,7 +137,8 @@ cudaError_t launch_phi8(const float* cand, long long n, int mode, float* out, in
     const unsigned blocks = (unsigned)((n + 255) / 256);
     if (blocks == 0) return cudaSuccess;
     if (mode == MEAN) tfn_phi8_kernel<MEAN><<<blocks, 256, 0, st>>>(cand, n, out, k_out);
-    else tfn_phi8_kernel<MEDIAN><<<blocks, 256, 0, st>>>(cand, n, out, k_out);
+    else if (mode == MEDIAN) tfn_phi8_kernel<MEDIAN><<<blocks, 256, 0, st>>>(cand, n, out, k_out);
+    else tfn_phi8_kernel<2><<<blocks, 256, 0, st>>>(cand, n, out, k_out);
     return cudaGetLastError();
 }
 

@@ -390,12 +390,14 @@ def stats(est: torch.Tensor, gt: torch.Tensor, layout: str = "planar", acc: Opti
 
 
 def debug_phi8(cand: torch.Tensor, nz_mode: str) -> Tuple[torch.Tensor, torch.Tensor]:
-    """P8 probe: device Phi of [n,8] candidates (non-finite = skipped)."""
+    """P8 probe: device Phi of [n,8] candidates (non-finite = skipped); nz_mode 'mean',
+    'median' or 'median_ext' (the strip kernel's fast-path median decision)."""
     _need(cand, "cand")
     n = cand.numel() // 8
     out = torch.empty(n, dtype=torch.float32, device=cand.device)
     k = torch.empty(n, dtype=torch.int32, device=cand.device)
-    _check(tfn_debug_phi8(cand.data_ptr(), n, MODES[nz_mode], out.data_ptr(), k.data_ptr(),
+    mode = 2 if nz_mode == "median_ext" else MODES[nz_mode]
+    _check(tfn_debug_phi8(cand.data_ptr(), n, mode, out.data_ptr(), k.data_ptr(),
                           _stream_ptr(None)), "tfn_debug_phi8")
     return out, k
 

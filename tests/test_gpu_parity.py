@@ -274,8 +274,11 @@ def test_phi8_probe(tfn):
     cc = torch.as_tensor(c).cuda()
     med, kk = tfn.debug_phi8(cc, "median")
     mean, _ = tfn.debug_phi8(cc, "mean")
+    mex, kx = tfn.debug_phi8(cc, "median_ext")      # the fast variants' NaN-propagating network
     med, kk, mean = med.cpu().numpy(), kk.cpu().numpy(), mean.cpu().numpy()
     assert np.array_equal(kk, np.isfinite(c).sum(1))
+    assert np.array_equal(kx.cpu().numpy(), kk)             # finite extremes <=> all 8 finite
+    assert np.array_equal(mex.cpu().numpy().view(np.uint32), med.view(np.uint32))
     for i in range(n):
         v = np.sort(c[i][np.isfinite(c[i])].astype(np.float64))
         if v.size == 0:
