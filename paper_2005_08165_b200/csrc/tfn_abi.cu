@@ -51,7 +51,7 @@ struct tfn_ctx {
     int strip_ctas_u16 = 0;                           // uint16 depth codes (general variant)
     int f32_ctas[2][2] = {{0, 0}, {0, 0}};            // fp32 unit-step kernel: [depth, disparity][fast, masked]
     int count_special = 0;               // TFN_OPT_COUNT_SPECIAL: fp32 kernel counts its special pixels
-    int* last_fired = nullptr;           //   (device counter of the last such launch)
+    std::atomic<int*> last_fired{nullptr};   //   (device counter of the last such launch)
     std::mutex ws_mu;
     Workspace ws;
     int* work = nullptr;                 // ring of per-call {work, fired} counter pairs
@@ -296,7 +296,7 @@ int run(tfn_handle h, const void* in, int in_u16, bool disp, int batch, int H, i
             if (cudaMemsetAsync(ctr, 0, 2 * sizeof(int), st) != cudaSuccess) return TFN_ERR_CUDA;
             a.work = dyn ? ctr : nullptr;
             a.fired = h->count_special ? ctr + 1 : nullptr;     // special pixels of this launch
-            h->last_fired = a.fired;
+            h->last_fired.store(a.fired);
         }
         if (tfn::launch_f32_any(tm, a, f32k, h->filter, h->mode, disp, vm, (int)ctas, st) != cudaSuccess)
             return TFN_ERR_CUDA;
@@ -729,11 +729,12 @@ TFN_API int tfn_debug_auto(int state, int probed, double rate, unsigned call, in
 TFN_API int tfn_debug_special_count(tfn_handle h, long long* count) {
     if (!h || !count) return TFN_ERR_INVALID_ARGUMENT;
     *count = -1;
-    if (!h->last_fired) return TFN_OK;
+    int* const lf = h->last_fired.load();
+    if (!lf) return TFN_OK;
     int n = 0;
-    if (cudaMemcpy(&n, h->last_fired, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return TFN_ERR_CUDA;
+    if (cudaMemcpy(&n, lf, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) return TFN_ERR_CUDA;
     *count = n;
     return TFN_OK;
 }
 
-TFN_API int tfn_version(void) { return 200; }
+TFN_API int tfn_version(void) { return 201; }
