@@ -632,6 +632,20 @@ def test_fd32_disparity_cancellation_fallback(tfn):
             assert_kernels_agree(g, gk, k in ("general", "pixel"), (kappa, k))
 
 
+def test_fd32_noisy_disparity(tfn, random8):
+    """noisy disparity (the high noise preset on the depth, then d = f b / Z) puts the FD32 sign
+    guard on a large share of pixels: the fallback runs for most row steps; parity and variant
+    agreement hold, with holes in the mix"""
+    z = ts.add_gaussian_noise(random8.depth[:2], ts.NOISE_PRESETS["high"], seed=11)
+    d = ts.depth_to_disparity(z.double(), 500.0, 0.12).numpy().astype(np.float32)
+    rng = np.random.default_rng(3)
+    d[rng.random(d.shape) < 0.02] = 0.0                     # holes (invalid disparity)
+    g, _ = check(tfn, d, ts.K_VGA, "fd", "mean", disp=True)
+    for k in ("masked", "general"):
+        gk = run_gpu(tfn, d, ts.K_VGA, "fd", "mean", disp=True, kernel=k)
+        assert_kernels_agree(g, gk, k == "general", k)
+
+
 def test_graph_counter_never_shared_with_direct_calls(tfn, random8):
     """a launch captured into a CUDA graph keeps its own work counter.  Capture a
     dynamically scheduled launch, make > 4096 direct calls (the direct-call ring wraps), then
