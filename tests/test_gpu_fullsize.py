@@ -2,8 +2,8 @@
 launch over the whole batch, default strip geometry, AUTO variant selection after the
 bench's warm-up calls), checked against the fp64 oracle on whole frames and on sampled
 pixels (the oracle finishes those in seconds).  configs[1] is in test_gpu_parity.py; this
-file covers configs[2] (disparity), configs[3] (1080p holes: AUTO -> general variant) and
-the N1 workload (uint16 codes -> half normals)."""
+file covers configs[2] (disparity), configs[3] (1080p holes: AUTO -> masked variant), the N1
+workload (uint16 codes -> half normals) and the FD launch configurations (16 warps/SM)."""
 import numpy as np
 import pytest
 import torch
@@ -117,3 +117,28 @@ def test_full_size_config6_u16_half(tfn):
         ref = oracle.estimate(z64, ts.K_VGA, "sobel", "median")
         res = compare(out[fi][None], ref[None], z64[None], ts.K_VGA, tol=TOL_F16_DEG)
         assert res["mask_equal"] and res["n_bad"] == 0, res
+
+
+@pytest.mark.parametrize("m,disp", [("mean", False), ("median", False), ("mean", True)])
+def test_full_size_fd_16_warps(tfn, m, disp):
+    """FD at full configs[1] / configs[2] size in the launch configuration bench.py times for
+    `--filter fd` (round 2: 16 warps/SM; FD + median through the TMA ring; disparity FD + mean
+    with fp32 gradients): one whole frame against the oracle, sampled pixels on two
+    more"""
+    n, H, W = 1024, 480, 640
+    sc = ts.random_scenes(n, ts.K_VGA, H, W, seed=0)
+    x = render_gpu(sc, ts.K_VGA, H, W, n, disp=disp)
+    est = tfn.Estimator(ts.K_VGA, "fd", m)
+    call = (lambda: est.estimate_disparity(x, F * B_)) if disp else (lambda: est.estimate(x))
+    warm(est, call)
+    out = call().cpu().numpy()
+    rng = np.random.default_rng(5)
+    for i, fi in enumerate((0, 511, 1023)):
+        r = ts.render(sc.subset(fi, fi + 1), ts.K_VGA, H, W, keep_depth64=disp)
+        frame = (ts.depth_to_disparity(r.depth64, F, B_) if disp else r.depth)[0].numpy()
+        assert np.array_equal(frame, x[fi].cpu().numpy())
+        if i == 0:
+            ref = oracle.estimate(frame, ts.K_VGA, "fd", m, disparity=disp, f_tc=F * B_, threads=8)
+            assert_parity(compare(out[fi][None], ref[None], frame[None], ts.K_VGA), f"fd/{m}/disp={disp} frame 0")
+        else:
+            sampled(out[fi], frame, ts.K_VGA, "fd", m, rng, disp=disp)
