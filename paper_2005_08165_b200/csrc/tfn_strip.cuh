@@ -19,7 +19,7 @@
 //          tau = fma(m Z_c, R, +-m), Phi (24-op median network with NaN-propagating
 //          min / max and an extreme-magnitude finiteness test / mean), n_z, normalise,
 //          orient — packed FMUL2/FFMA2/FADD2 over pixel pairs (0,1), (2,3).
-//   FD32:  disparity FD + mean fast / masked only — the gradients in fp32.
+//   FD32:  disparity FD fast / masked only — the gradients in fp32.
 // Three variants (KV), bit-identical, picked at run time by AUTO (tfn_abi.cu):
 //   fast (0):    all 8 candidates finite and Phi != 0 (no skips, no flat rule, no
 //                orientation tie, valid pixel) in registers; anything else ("special":
@@ -48,7 +48,7 @@
 #define TFN_PHI_EXT 1            // median fast / masked: finiteness from the network's extremes, no candidate sum
 #endif
 #ifndef TFN_FD32
-#define TFN_FD32 1               // disparity FD + mean fast / masked: fp32 gradients (FD32_ON, fd_dw)
+#define TFN_FD32 1               // disparity FD fast / masked: fp32 gradients (FD32_ON, fd_dw)
 #endif
 #ifndef TFN_STRIP_TMA
 #define TFN_STRIP_TMA 1          // fp32 input rows through the per-warp TMA ring (tfn_tma.cuh) instead of
@@ -349,13 +349,13 @@ constexpr bool TMA_ON = (TFN_STRIP_TMA != 0) && (sizeof(T) == 4) &&
                         (TFN_STRIP_TMA_ALL || (TFN_FD_MEDIAN16 && F == FD && !GEN) ||
                          (!(MODE == MEDIAN && !GEN && !VM) && !(MODE == MEAN && GEN)));
 
-// FD32 (fast / masked FD + mean on fp32 disparity): the gradients in fp32 (fd_dw below) — no fp64,
-// no F2F on the XU, which bounds the mean mode.  Measured (r02, configs[1]-sized batches):
-// disparity FD + mean 312 -> 336 Gpx/s; on depth each difference costs 3 fp32 ops instead of
-// one fp64 subtraction (91 vs 77 instr/px: 265 vs 291 Gpx/s) and the median is issue-bound
-// (182 vs 220), so those keep the fp64 path
+// FD32 (fast / masked FD on fp32 disparity): the gradients in fp32 (fd_dw below) — no fp64, no
+// F2F on the XU, which bounds the mean mode.  Measured (r02, configs[1]-sized batches):
+// disparity FD + mean 312 -> 336 Gpx/s, FD + median 252 -> 255; on depth each difference costs
+// 3 fp32 ops instead of one fp64 subtraction (91 vs 77 instr/px: 265 vs 291 Gpx/s; median 182
+// vs 220), so depth keeps the fp64 path
 template <int F, int MODE, bool DISP, bool GEN, class T>
-constexpr bool FD32_ON = TFN_FD32 && F == FD && MODE == MEAN && DISP && !GEN && sizeof(T) == 4;
+constexpr bool FD32_ON = TFN_FD32 && F == FD && DISP && !GEN && sizeof(T) == 4;
 
 // w_b - w_a for two samples: disparity x = d, so d_b - d_a; depth x = 1/z, so
 // (z_a - z_b) w_a w_b — the difference of the samples is exact (Sterbenz) or rounded once, and

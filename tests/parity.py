@@ -70,14 +70,14 @@ def assert_parity(res: dict, what: str = ""):
 
 
 # Kernel-variant agreement.  Every variant computes bit-identical normals except the fast /
-# masked variants of disparity FD + mean, whose gradients are fp32 (FD32) while the
+# masked variants of disparity FD (mean and median), whose gradients are fp32 (FD32) while the
 # general and per-pixel kernels keep the fp64 path: those agree to FD32_TOL_DEG with identical
 # invalid masks (each is separately within TOL_DEG of the oracle).
 FD32_TOL_DEG = 5e-5
 
 
-def fd32_variant(disp: bool, f, m) -> bool:
-    return bool(disp) and f == "fd" and m == "mean"
+def fd32_variant(disp: bool, f, m=None) -> bool:
+    return bool(disp) and f == "fd"
 
 
 def assert_kernels_agree(a: np.ndarray, b: np.ndarray, loose: bool = False, what=""):

@@ -617,7 +617,7 @@ def test_extreme_disparity_and_noise(tfn, random8, scale):
 
 
 def test_fd32_disparity_cancellation_fallback(tfn):
-    """disparity FD + mean runs fp32 gradients with s and t re-paired along the diagonals; a
+    """disparity FD runs fp32 gradients with s and t re-paired along the diagonals; a
     saddle d = 1 + 1e-2 (u - v) + kappa (u + v)^2 puts s = g_u + g_v through zero along u + v = c,
     where the two diagonal differences have opposite signs and the pixel takes the fp64 s, t
     (fd_st64): parity with the oracle on both sides of the line, every variant, three curvatures"""
@@ -626,10 +626,11 @@ def test_fd32_disparity_cancellation_fallback(tfn):
     for kappa in (1e-6, 1e-5, 1e-4):
         d = 2.0 + 1e-2 * (u - v) + kappa * (u + v - 120.0) ** 2
         d = d.astype(np.float32)[None]
-        g, _ = check(tfn, d, ts.K_VGA, "fd", "mean", disp=True)
-        for k in ("masked", "general", "pixel"):
-            gk = run_gpu(tfn, d, ts.K_VGA, "fd", "mean", disp=True, kernel=k)
-            assert_kernels_agree(g, gk, k in ("general", "pixel"), (kappa, k))
+        for m in MODES:
+            g, _ = check(tfn, d, ts.K_VGA, "fd", m, disp=True)
+            for k in ("masked", "general", "pixel"):
+                gk = run_gpu(tfn, d, ts.K_VGA, "fd", m, disp=True, kernel=k)
+                assert_kernels_agree(g, gk, k in ("general", "pixel"), (kappa, m, k))
 
 
 def test_fd32_noisy_disparity(tfn, random8):
@@ -640,10 +641,11 @@ def test_fd32_noisy_disparity(tfn, random8):
     d = ts.depth_to_disparity(z.double(), 500.0, 0.12).numpy().astype(np.float32)
     rng = np.random.default_rng(3)
     d[rng.random(d.shape) < 0.02] = 0.0                     # holes (invalid disparity)
-    g, _ = check(tfn, d, ts.K_VGA, "fd", "mean", disp=True)
-    for k in ("masked", "general"):
-        gk = run_gpu(tfn, d, ts.K_VGA, "fd", "mean", disp=True, kernel=k)
-        assert_kernels_agree(g, gk, k == "general", k)
+    for m in MODES:
+        g, _ = check(tfn, d, ts.K_VGA, "fd", m, disp=True)
+        for k in ("masked", "general"):
+            gk = run_gpu(tfn, d, ts.K_VGA, "fd", m, disp=True, kernel=k)
+            assert_kernels_agree(g, gk, k == "general", (m, k))
 
 
 def test_graph_counter_never_shared_with_direct_calls(tfn, random8):
