@@ -337,7 +337,9 @@ __device__ __forceinline__ void store_packed(__half* o, const float* x, const fl
 // median fast 211 (TMA) vs 218 (register prefetch), masked 211 vs 212, general 176 vs 172; mean
 // fast 261 vs 252, masked 263 vs 247, general 168 vs 177 Gpx/s — the register window already
 // loads every sample once (loads are 1/4 of the traffic), so the ring only removes the prefetch
-// registers; it stays off where it measured slower (fast median, general mean).
+// registers; it stays off where it measured slower (fast and masked median — configs[3], the
+// masked variant's workload: 203.2 vs 199.6 — and general mean), except FD median, whose
+// freed registers buy 16 warps/SM.
 #ifndef TFN_STRIP_TMA_ALL
 #define TFN_STRIP_TMA_ALL 0      // 1: every fp32 variant through the ring (A/B builds)
 #endif
@@ -347,7 +349,7 @@ __device__ __forceinline__ void store_packed(__half* o, const float* x, const fl
 template <int F, class T, int MODE, bool GEN, bool VM>
 constexpr bool TMA_ON = (TFN_STRIP_TMA != 0) && (sizeof(T) == 4) &&
                         (TFN_STRIP_TMA_ALL || (TFN_FD_MEDIAN16 && F == FD && !GEN) ||
-                         (!(MODE == MEDIAN && !GEN && !VM) && !(MODE == MEAN && GEN)));
+                         (!(MODE == MEDIAN && !GEN) && !(MODE == MEAN && GEN)));
 
 // FD32 (fast / masked FD on fp32 disparity): the gradients in fp32 (fd_dw below) — no fp64, no
 // F2F on the XU, which bounds the mean mode.  Measured (r02, configs[1]-sized batches):
