@@ -31,10 +31,10 @@
 #endif
 
 #ifndef TFN_RING_RC
-#define TFN_RING_RC 4             // rows per TMA box
+#define TFN_RING_RC 8             // rows per TMA box (r02 A/B: 8 x 2 slots beats 4 x 4 by 1-2 %, same shared memory)
 #endif
 #ifndef TFN_RING_NS
-#define TFN_RING_NS 4             // slots per warp
+#define TFN_RING_NS 2             // slots per warp
 #endif
 
 namespace tfn {
