@@ -196,6 +196,14 @@ def test_sizes(tfn, H, W):
             if W % 4 == 0 and W >= 4:
                 gp = run_gpu(tfn, z, K, f, m, kernel="pixel")
                 assert np.array_equal(g.view(np.uint32), gp.view(np.uint32))
+    # disparity (the FD32 path; Eq. 21 needs fx == fy)
+    Kd = ts.Intrinsics(205.0, 205.0, W / 2 - 0.3, H / 2 + 0.7)
+    d = np.where(z > 0, 60.0 / np.where(z > 0, z, 1.0), 0.0).astype(np.float32)
+    for m in MODES:
+        g, _ = check(tfn, d, Kd, "fd", m, disp=True)
+        if W % 4 == 0 and W >= 4:
+            gp = run_gpu(tfn, d, Kd, "fd", m, disp=True, kernel="pixel")
+            assert_kernels_agree(g, gp, True, (H, W, m))
 
 
 def test_depth_scale_power_of_two_bitwise(tfn, cfg1):
