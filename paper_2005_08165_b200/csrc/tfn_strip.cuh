@@ -39,7 +39,7 @@
 #define TFN_U16_MINBLOCKS 4      // resident CTAs per SM of the uint16 (ring) instantiations (128 registers: +2.3 % over 3)
 #endif
 #ifndef TFN_CPA_D
-#define TFN_CPA_D 6              // cp.async ring prefetch distance (rows), <= 8
+#define TFN_CPA_D 4              // cp.async ring prefetch distance (rows), <= 8 (r02 A/B on config 6: 4 > 8 > 6 by ~1 %)
 #endif
 #ifndef TFN_STRIP_PPL
 #define TFN_STRIP_PPL 4          // pixels (columns) per lane: 4 or 2
