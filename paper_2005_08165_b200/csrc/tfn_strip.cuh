@@ -758,7 +758,7 @@ template <int F, int MODE, int KV, class T>
 constexpr int strip_minblocks() {
     return Ring<T, KV == 1>::on ? TFN_U16_MINBLOCKS
            : (F == FD && MODE == MEAN && KV != 1) ? TFN_STRIP_MINBLOCKS_FDMEAN
-           : (TFN_FD_MEDIAN16 && F == FD && KV != 1) ? 4 : TFN_STRIP_MINBLOCKS;
+           : (TFN_FD_MEDIAN16 && F == FD && KV != 1) ? TFN_STRIP_MINBLOCKS_FDMEAN : TFN_STRIP_MINBLOCKS;
 }
 
 // KV (kernel variant): 0 fast path + exact per-pixel special path, 1 general (no special
