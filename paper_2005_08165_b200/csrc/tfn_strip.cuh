@@ -5,9 +5,9 @@
 // frame; each lane owns PPL adjacent columns and walks down the strip with a rolling
 // window of three row "slots" (rows v-1, v, v+1).  The row loop is unrolled by 3 and the
 // slots rotate by renaming (no register copies).  Per lane-row, fp32 input: rows of 136
-// columns x 4 arrive as TMA boxes in a per-warp shared-memory ring (tfn_tma.cuh; the fast
-// median variant instead loads one LDG.128 + two predicated halo loads three rows ahead into
-// registers — measured faster there); uint16 input: one cp.async of 8 B into a per-warp ring
+// columns x 8 arrive as TMA boxes in a per-warp shared-memory ring (tfn_tma.cuh; the fast and
+// masked median variants instead load one LDG.128 + two predicated halo loads three rows
+// ahead into registers — measured faster there, except FD); uint16 input: one cp.async of 8 B into a per-warp ring
 // TFN_CPA_D rows ahead (halo words by the edge lanes), read back with LDS; out: three STG.128
 // (fp32) / STG.64 (half) / one or two vector stores (oct16).  Persistent grid (12 warps/SM;
 // FD + mean 16); strips handed out by an atomic work counter (dynamic scheduling).
@@ -748,11 +748,11 @@ __device__ __forceinline__ void strip_rows(const StripCtx<T>& c, char* out, long
 }
 
 // resident CTAs per SM the register budget is sized for: 3 (168 registers, 12 warps) by
-// default; the uint16 ring instantiations 4 (128); the fp32 FD + mean fast / masked
-// instantiations TFN_STRIP_MINBLOCKS_FDMEAN (no median network, no corner taps: the only ones
-// that fit 128 registers without spills)
+// default; the uint16 ring instantiations 4 (128); the fp32 FD fast / masked instantiations
+// TFN_STRIP_MINBLOCKS_FDMEAN (no corner taps: with the TMA ring for the median they are the
+// only ones that fit 128 registers without spills)
 #ifndef TFN_STRIP_MINBLOCKS_FDMEAN
-#define TFN_STRIP_MINBLOCKS_FDMEAN 4        // measured: FD + mean 274.5 -> 290.7 Gpx/s (16 vs 12 warps/SM; XU-bound, r02)
+#define TFN_STRIP_MINBLOCKS_FDMEAN 4        // measured: FD + mean 274.5 -> 290.7, FD + median 220 -> 231 Gpx/s (16 vs 12 warps/SM, r02)
 #endif
 template <int F, int MODE, int KV, class T>
 constexpr int strip_minblocks() {
